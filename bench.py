@@ -1,0 +1,352 @@
+"""Benchmark: ray-bounce segments/s into SH energy IRs (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+One step = one frame of the configured workload (default C2, BASELINE.json
+configs[1]: 2,402-triangle procedural city, 8 sources x 32,768 paths, 100
+bounces, order-3 SH histogram, 4 bands): ef_trace (one persistent kernel
+over all paths of all sources, histogram cleared by DMA first) followed by
+ef_analyze (per-band RT60/DRR/predelay/loudness).  N > 1 (torchrun): weak
+scaling, every rank traces its own 32,768-ray slice of every source
+(global ray index = rank * R + i) and the partial histograms are summed with
+one NCCL reduce-scatter per frame, each rank then analysing S/N sources.
+
+Timing: CUDA events per step on the launching stream, L2 flushed (256 MiB
+write) between steps outside the events, max over ranks.  ``e2e`` repeats
+the steps through the public API with pinned host inputs/outputs and the
+copies inside the timed region.  ``--impl reference`` times the CPU oracle
+port of the reference algorithm (oracle/efo.c, every host core) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic work per segment of the REFERENCE algorithm (tools/measure_work.py,
+# DESIGN.md section 5): nodes visited / triangles tested by bvh.py:130-160
+# (C1: all-pairs over 12 triangles), listener-arrival fraction.
+WORK = {
+    "c1": dict(N_node=0.0, N_tri=12.0, P_arr=0.011300),
+    "c2": dict(N_node=32.304, N_tri=5.334, P_arr=0.0),
+}
+
+
+def b_seg(cfg, n_bands, nk):
+    w = WORK[cfg]
+    return 72 * w["N_tri"] + 32 * w["N_node"] + (28 + 8 * n_bands) + w["P_arr"] * 8 * n_bands * nk
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                sm, smax, reasons = [x.strip() for x in out.split(",")]
+                self.samples.append((float(sm), float(smax), int(reasons, 16)))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+        bits = 0
+        for s in self.samples:
+            bits |= s[2]
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [v for k, v in names.items() if bits & k and k != 0x1],
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------- CPU arm
+def cpu_oracle_rate(w, rays_per_source, threads):
+    """CPU port of the reference algorithm (oracle/efo.c, reference BVH and
+    traversal, the pinned bounce loop) on `threads` host threads: each thread
+    traces a contiguous ray shard of every source.  Returns (seg/s, segs, s)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    os_ = O.OracleScene.from_arrays(w.arrays())
+    bin_len = w.speed_of_sound * w.bin_s
+    shards = []
+    per = max(1, rays_per_source // threads)
+    for s in range(len(w.sources)):
+        for r0 in range(0, rays_per_source, per):
+            shards.append((s, r0, min(per, rays_per_source - r0)))
+
+    def run(job):
+        s, r0, n = job
+        r = O.trace(os_, src_key=s, src_pos=w.sources[s], listener=w.listener, radius=w.radius,
+                    seed=w.seed, order=w.order, n_bins=w.n_bins, bin_len=bin_len,
+                    max_bounces=w.max_bounces, e0=1.0, ray0=r0, n_rays=n)
+        return r.stats["segments"]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        segs = sum(ex.map(run, shards))
+    dt = time.perf_counter() - t0
+    return segs / dt, segs, dt
+
+
+def run_reference(args, w, metric, unit):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    rays = max(1, int(w.n_rays * args.cpu_fraction))
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_oracle_rate(w, max(1, rays // 16), cores)
+    rates, secs = [], []
+    for _ in range(args.steps):
+        r, segs, dt = cpu_oracle_rate(w, rays, cores)
+        rates.append(r)
+        secs.append(dt)
+    value = float(np.median(rates))
+    sample = f"rays [0,{rays}) of each of the {len(w.sources)} sources of {w.name} per step"
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, w, world),
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, w, world):
+    return {"workload": f"{w.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c5': 4}[args.config] }])",
+            "triangles": int(w.n_tri), "sources": int(len(w.sources)),
+            "rays_per_source_per_rank": int(w.n_rays), "max_bounces": int(w.max_bounces),
+            "sh_order": int(w.order), "bands": int(w.n_bands), "bins": int(w.n_bins),
+            "parallelism": f"rays sharded x{world}, NCCL reduce-scatter of histograms" if world > 1
+            else "single GPU", "l2": "flushed between steps (256 MiB write)"}
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_gpu(args, w, metric, unit):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_00430_b200 import _lib
+    from paper_1803_00430_b200.analysis import Analyzer
+    from paper_1803_00430_b200.propagation import FrameTracer, TraceConfig
+    from paper_1803_00430_b200.scene import scene_from_workload
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    sc = scene_from_workload(w)
+    S = len(w.sources)
+    cfg = TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                      bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = FrameTracer(sc, S, cfg)
+    tr.set_sources(w.sources)
+    if world > 1 and S % world:
+        raise SystemExit("sources must divide by the number of ranks")
+    S_own = S // world
+    an = Analyzer(S_own, w.n_bins, sc.n_bands, w.order, w.bin_s)
+    nk = cfg.n_coeffs
+    if world > 1:
+        H_own = torch.empty((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
+        D_own = torch.empty((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
+        st_own = torch.empty((S_own, tr.stats.shape[1]), dtype=torch.int64, device=dev)
+        su_own = torch.empty((S_own,), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    total_rays = w.n_rays * world
+    ray0 = rank * w.n_rays
+
+    k_start = torch.cuda.Event(enable_timing=True)
+    k_end = torch.cuda.Event(enable_timing=True)
+
+    def step(kernel_events=None):
+        if kernel_events:
+            kernel_events[0].record(stream)
+        tr.trace(w.listener, ray0=ray0, total_rays=total_rays)
+        if kernel_events:
+            kernel_events[1].record(stream)
+        if world > 1:
+            dist.reduce_scatter_tensor(H_own, tr.H)
+            dist.reduce_scatter_tensor(D_own, tr.Dir)
+            dist.reduce_scatter_tensor(st_own, tr.stats)
+            dist.reduce_scatter_tensor(su_own, tr.sum_t)
+            an.run(H_own, D_own, st_own, su_own)
+        else:
+            an.run(tr.H, tr.Dir, tr.stats, tr.sum_t)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    segs_per_step = int(tr.stats[:, 1].sum().item())   # this rank's segments (deterministic)
+    arrivals = int(tr.stats[:, 3].sum().item())
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = _lib.launch_count()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)                 # evict L2 (126 MB) outside the timed events
+            starts[i].record(stream)
+            step(kev[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_launch = _lib.launch_count() - n_launch0
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    k_ms = sum(a.elapsed_time(b) for a, b in kev)
+    segs_check = int(tr.stats[:, 1].sum().item())
+    assert segs_check == segs_per_step, "segment count changed between steps"
+
+    # ---- e2e through the public API: pinned host in/out, copies timed
+    src_host = torch.from_numpy(np.ascontiguousarray(w.sources, np.float64)).pin_memory()
+    H_host = torch.empty(tuple(an.params.shape), dtype=torch.float64).pin_memory()
+    Hist_host = torch.empty(tuple((H_own if world > 1 else tr.H).shape), dtype=torch.float32).pin_memory()
+    e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        e_starts[i].record(stream)
+        tr.src_pos.copy_(src_host, non_blocking=True)
+        step()
+        Hist_host.copy_(H_own if world > 1 else tr.H, non_blocking=True)
+        H_host.copy_(an.params, non_blocking=True)
+        e_ends[i].record(stream)
+    torch.cuda.synchronize()
+    e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
+    h2d = src_host.numel() * 8
+    d2h = Hist_host.numel() * 4 + H_host.numel() * 8
+
+    # ---- max over ranks, totals over ranks
+    t = torch.tensor([ms, k_ms, e_ms], dtype=torch.float64, device=dev)
+    segs = torch.tensor([segs_per_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(segs, op=dist.ReduceOp.SUM)
+    ms, k_ms, e_ms = (float(x) for x in t.cpu())
+    total_segs = float(segs.item()) * args.steps
+    value = total_segs / (ms * 1e-3)
+    e2e_value = total_segs / (e_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (trace): algorithmic bytes / launch
+    peak, peak_kind = measured_peaks()
+    bseg = b_seg(args.config, sc.n_bands, nk)
+    avg_k_s = (k_ms * 1e-3) / args.steps
+    achieved = bseg * segs_per_step / avg_k_s / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    if rank != 0:
+        return
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, w, world),
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps},
+            "gpu_launches": int(n_launch),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "trace_kernel", "kernel_ms_per_launch": avg_k_s * 1e3,
+                         "algorithmic_bytes_per_segment": bseg,
+                         "segments_per_launch": segs_per_step},
+            "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
+            "clocks": clocks.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        rays = max(1, int(w.n_rays * args.cpu_fraction))
+        rate, segs_c, dt = cpu_oracle_rate(w, rays, cores)
+        line["cpu_baseline"] = {"value": rate, "unit": unit, "cores": cores, "kind": "port",
+                                "sample": f"rays [0,{rays}) of each of the {len(w.sources)} sources "
+                                          f"({segs_c} segments, {dt:.2f} s)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(WORK))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-fraction", type=float, default=1.0,
+                    help="fraction of each source's rays in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    from paper_1803_00430_b200 import workloads
+    w = workloads.WORKLOADS[args.config]()
+    metric = "ray-bounce segments/sec into SH energy IRs"
+    unit = "segments/s"
+    if args.impl == "reference":
+        run_reference(args, w, metric, unit)
+    else:
+        run_gpu(args, w, metric, unit)
+
+
+if __name__ == "__main__":
+    main()

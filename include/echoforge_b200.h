@@ -1,0 +1,204 @@
+/*
+ * echoforge_b200.h -- C ABI of the B200-native hot path of the echoforge
+ * reference (arXiv 1803.00430; /root/reference/pkg/src/echoforge).
+ *
+ * The reference has no FFI: its boundary is the Python call signatures of
+ * scene.py / bvh.py / sh.py plus the SPEC-only propagation and ir-analysis
+ * operations.  Every entry point below replaces one of them (cited per
+ * function); the Python package paper_1803_00430_b200 binds them with ctypes
+ * and keeps the reference signatures.
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no torch types.  "host" pointers are CPU
+ *     memory, "device" pointers are CUDA global memory on the current device.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and never blocks the host unless documented.
+ *   - Return 0 (EF_OK) or a negative status; never throws, never exits.  The
+ *     message of the last failure on the calling thread is available through
+ *     ef_last_error().  Contract violations -> EF_EINVAL (Python: ValueError),
+ *     CUDA failures -> EF_ECUDA (Python: RuntimeError).
+ *   - ef_scene handles are immutable after ef_scene_create and may be used
+ *     concurrently from several streams.
+ */
+#ifndef ECHOFORGE_B200_H
+#define ECHOFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EF_OK 0
+#define EF_EINVAL (-1)
+#define EF_ECUDA (-2)
+#define EF_ENOMEM (-3)
+#define EF_EUNSUPPORTED (-4)
+
+#define EF_ABI_VERSION 1
+
+/* Per-source trace counters (u64), index into the stats array. */
+enum {
+    EF_ST_PATHS = 0,       /* primary rays traced                               */
+    EF_ST_SEGMENTS,        /* closest-hit queries (the throughput unit)         */
+    EF_ST_REFLECTIONS,     /* segments that ended on a surface                  */
+    EF_ST_ARRIVALS,        /* listener-sphere crossings                         */
+    EF_ST_DIRECT,          /* crossings before any reflection (-> Dir)          */
+    EF_ST_DROPPED,         /* late arrivals past the IR length    */
+    EF_ST_ESCAPED,         /* paths that left the scene                         */
+    EF_ST_COUNT = 8
+};
+
+/* Per-(source, band) analysis outputs (f64), index into params. */
+enum {
+    EF_P_RT60 = 0,         /* s, clamped to [0.05, max_rt]   */
+    EF_P_GAIN,             /* g_reverb                        */
+    EF_P_DRR_DB,           /* 10 log10(E_dir / E_reverb), +-99 dB clamps        */
+    EF_P_TOTAL,            /* sum_t I_b(t)                                      */
+    EF_P_DIRECT,           /* E_dir,b                                           */
+    EF_P_SILENT,           /* 1.0 if the band is silent / indeterminate         */
+    EF_P_FIT_N,            /* bins used by the decay regression                 */
+    EF_P_SLOPE,            /* dB/s                                              */
+    EF_P_COUNT = 8
+};
+/* Per-source analysis outputs (f64). */
+enum {
+    EF_S_PREDELAY = 0,     /* s, -1 when silent               */
+    EF_S_MFP,              /* mean free path, m               */
+    EF_S_SILENT,
+    EF_S_COUNT = 4
+};
+
+typedef struct ef_scene ef_scene;
+
+/* ---- library -------------------------------------------------------- */
+int ef_abi_version(void);
+/* Copies the calling thread's last error message (NUL-terminated). */
+int ef_last_error(char* buf, size_t n);
+/* Number of CUDA kernels this library launched since load (all threads). */
+uint64_t ef_launch_count(void);
+
+/* ---- scene ------------------------------------------------------------
+ * Replaces SceneModel.__init__ (scene.py:149-171) and BVH.__init__
+ * (bvh.py:51-128).  All inputs are HOST arrays, copied: v0/e1/e2/normals
+ * (n_tri,3) f64 exactly as the reference stores them (scene.py:152-166),
+ * material_index (n_tri,) i64, absorption/scattering (n_materials, n_bands)
+ * f64 in [0,1] (scene.py:167-170; n_bands generalised from 4 to 1..8).
+ * Builds the device BVH (binned SAH, 64-byte two-child nodes, conservative
+ * f32 boxes) and uploads the f64 triangle payload in leaf order. */
+int ef_scene_create(const double* v0, const double* e1, const double* e2,
+                    const double* normals, const int64_t* material_index, int64_t n_tri,
+                    const double* absorption, const double* scattering,
+                    int32_t n_materials, int32_t n_bands, ef_scene** out);
+int ef_scene_destroy(ef_scene* scene);
+/* out[0]=n_tri out[1]=n_nodes out[2]=max_depth out[3]=device bytes
+ * out[4]=max leaf size out[5]=n_bands out[6]=n_materials */
+int ef_scene_info(const ef_scene* scene, int64_t* out7);
+
+/* ---- ray queries ------------------------------------------------------
+ * Replaces SceneModel.intersect_batch (scene.py:208-230), BVH.intersect
+ * (bvh.py:130-160, one ray per row) and SceneModel.intersect_brute
+ * (scene.py:194-206).  DEVICE arrays: origins, dirs (n,3) f64; t_max (n,)
+ * f64 or NULL (= +inf); outputs t (n,) f64 (+inf on miss), tri (n,) i64 (-1),
+ * hit (n,) u8.  mode: 0 = reference dispatch (all-pairs for n_tri <= 512,
+ * else BVH), 1 = all triangles, 2 = BVH.  Ties in t resolve to the lowest
+ * triangle id (the reference's all-pairs rule, scene.py:220). */
+int ef_intersect_batch(const ef_scene* scene, const double* origins, const double* dirs,
+                       int64_t n, double t_min, const double* t_max, int32_t mode,
+                       double* t_out, int64_t* tri_out, uint8_t* hit_out, void* stream);
+
+/* Replaces SceneModel.occluded_batch (scene.py:232-252): DEVICE origins,
+ * targets (n,3) f64 -> out (n,) u8, 1 where the segment is blocked. */
+int ef_occluded_batch(const ef_scene* scene, const double* origins, const double* targets,
+                      int64_t n, uint8_t* out, void* stream);
+
+/* Replaces ray_triangles (bvh.py:11-28) and ray_triangles_batch
+ * (bvh.py:31-45): every ray against every triangle.  DEVICE origins, dirs
+ * (n_rays,3); v0, e1, e2 (n_tri,3) f64; t_max (n_rays,) or NULL (= none, the
+ * batch form).  Outputs t (n_rays, n_tri) f64 -- including the reference's
+ * values for invalid pairs (0 when |det| <= 1e-14) -- and valid (n_rays,
+ * n_tri) u8 = barycentric test && t > t_min && t <= t_max. */
+int ef_ray_triangles(const double* origins, const double* dirs, int64_t n_rays,
+                     const double* v0, const double* e1, const double* e2, int64_t n_tri,
+                     double t_min, const double* t_max, double* t_out, uint8_t* valid_out,
+                     void* stream);
+
+/* ---- spherical harmonics ---------------------------------------------
+ * Replaces eval_sh_batch (sh.py:86-126): DEVICE dirs (n,3) f64 -> out
+ * (n,(order+1)^2) f64, bit-identical to the reference; order 0..4. */
+int ef_eval_sh_batch(const double* dirs, int64_t n, int32_t order, double* out, void* stream);
+
+/* Replaces directional_loudness_matrix (sh.py:240-253) for n
+ * distributions: DEVICE avg (n,(order+1)^2) f64, design (n_design,3) f64 ->
+ * out (n, nk, nk) f64 = (4 pi / N) B^T diag(max(0, B avg)) B. */
+int ef_loudness_batch(const double* avg, int64_t n, int32_t order, const double* design,
+                      int32_t n_design, double* out, void* stream);
+
+/* ---- propagation ------------------------------------------------------
+ * Replaces trace_frame for n_sources sources in one
+ * launch (forward tracing from point sources to a listener sphere, the
+ * BASELINE.json configs).  Bounce model pinned in DESIGN.md section 3. */
+typedef struct {
+    int32_t n_sources;
+    int32_t order;          /* SH order of the histogram, 0..4              */
+    int32_t n_bins;         /* IR length in bins                           */
+    int32_t max_bounces;    /* reflections per path                        */
+    int64_t n_rays;         /* rays per source traced by this call         */
+    uint32_t ray0;          /* global index of the first ray (sharding)    */
+    uint32_t seed;          /* Philox key word 0                           */
+    uint32_t frame;         /* Philox counter word 3                       */
+    int32_t mode;           /* 0 reference dispatch, 1 all-pairs, 2 BVH     */
+    double bin_len;         /* metres of path per bin = c * bin_seconds    */
+    double listener[3];
+    double radius;          /* listener sphere radius, m                   */
+    float e0;               /* initial energy per band of every path       */
+    int32_t record_ids;     /* nonzero: write per-segment hit ids          */
+    int32_t clear_outputs;  /* nonzero: zero H, Dir, stats, sum_t first    */
+    int32_t reserved;
+} ef_trace_config;
+
+/* DEVICE arrays:
+ *   src_pos  (n_sources,3) f64      src_key (n_sources,) u32 Philox key word 1
+ *   ray_ids  (n_rays,) u32 or NULL: explicit global ray indices (subsets)
+ *   H        (n_sources, n_bins, n_bands, nk) f32, ACCUMULATED (caller zeroes)
+ *   Dir      (n_sources, n_bands, nk) f32, ACCUMULATED direct arrivals
+ *   stats    (n_sources, EF_ST_COUNT) u64, ACCUMULATED
+ *   sum_t    (n_sources,) f64, ACCUMULATED reflected segment lengths
+ *   path_nseg (n_sources*n_rays,) i32 or NULL: segments per path
+ *   path_ids (n_sources*n_rays, max_bounces) i32 or NULL: hit ids (-1 escape)
+ * nk = (order+1)^2. */
+int ef_trace(const ef_scene* scene, const ef_trace_config* cfg, const double* src_pos,
+             const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
+             unsigned long long* stats, double* sum_t, int32_t* path_nseg, int32_t* path_ids,
+             void* stream);
+
+/* ---- ir-analysis ------------------------------------------------------
+ * Replaces estimate_rt60, reverb_gain (290),
+ * estimate_predelay (299), average_directivity (308) and
+ * directional_loudness_matrix (sh.py:240-253), batched over sources and
+ * bands.  DEVICE inputs are ef_trace's outputs; design (n_design,3) f64 is
+ * the t-design of design_for_order(order) (tdesigns.py:360).
+ * Outputs (DEVICE): params (n_sources, n_bands, EF_P_COUNT) f64,
+ * src_params (n_sources, EF_S_COUNT) f64, avg_dir (n_sources, n_bands, nk)
+ * f64, loudness (n_sources, n_bands, nk, nk) f64 or NULL. */
+typedef struct {
+    int32_t n_sources, n_bins, n_bands, order;
+    double bin_s;           /* seconds per bin                             */
+    double max_rt;          /* RT60 clamp upper bound, s                   */
+} ef_analysis_config;
+
+int ef_analyze(const ef_analysis_config* cfg, const float* H, const float* Dir,
+               const unsigned long long* stats, const double* sum_t, const double* design,
+               int32_t n_design, double* params, double* src_params, double* avg_dir,
+               double* loudness, void* stream);
+
+/* Replaces accumulate_ir: DEVICE f32 arrays of n
+ * elements, out = alpha * frame + (1 - alpha) * cache (out may alias). */
+int ef_blend(const float* cache, const float* frame, int64_t n, double alpha, float* out,
+             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECHOFORGE_B200_H */

@@ -253,6 +253,8 @@ def main():
     for i in range(100):
         h = box.intersect(origins[i], dirs[i])
         st[i], stri[i] = h.distance, h.triangle
+    rt_t, rt_v = ref_bvh.ray_triangles_batch(origins, dirs, box.v0, box.e1, box.e2, 1e-4)
+    rs_t, rs_v = ref_bvh.ray_triangles(origins[3], dirs[3], box.v0, box.e1, box.e2, 1e-4, 7.5)
     special_o = np.array([[0.0, 0, 0], [5.0, 0, 0], [0.0, 0, 0]])
     special_d = np.array([[1.0, 0, 0], [1.0, 0, 0], [0.0, 0, 1.0]])
     sp = [box.bvh.intersect(special_o[i], special_d[i], 1e-4, np.inf) for i in range(3)]
@@ -262,7 +264,7 @@ def main():
              origins=origins, dirs=dirs, t=t, tri=tri, hit=hit, scalar_t=st, scalar_tri=stri,
              special_o=special_o, special_d=special_d,
              special_t=np.array([s[0] for s in sp]), special_tri=np.array([s[1] for s in sp]),
-             **_bvh_arrays(box))
+             rt_t=rt_t, rt_valid=rt_v, rs_t=rs_t, rs_valid=rs_v, **_bvh_arrays(box))
 
     # --- 700-triangle soup, seed 7 (test_scene.py:145-169) ---------------------
     rng = np.random.default_rng(7)

@@ -1,0 +1,264 @@
+// K4: per-(source, band) decay-fit reducer.  One CTA per source, one warp
+// per band; every reduction is a warp-level segmented sum in f64.
+//
+// Replaces (SPEC-only in the reference, pinned in DESIGN.md 3.6):
+//   estimate_rt60           SPEC.md:272-280 (decisions 344-346)
+//   reverb_gain
+//   estimate_predelay       SPEC.md:299-307 (decision 347)
+//   average_directivity
+//   mean free path
+// and the reference's directional_loudness_matrix (sh.py:240-253) on
+// design_for_order(order) (tdesigns.py:360-362).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "ef_device.cuh"
+
+namespace ef {
+
+constexpr unsigned kAll = 0xffffffffu;
+constexpr double kY00 = 0.28209479177387814;   // sh.py:17
+constexpr int kMaxDesign = 64;    // design_for_order(<=4) has 48 points
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kAll, v, o);
+    return v;
+}
+
+struct AnalyzeParams {
+    const float* H;
+    const float* Dir;
+    const unsigned long long* stats;
+    const double* sum_t;
+    const double* design;
+    int32_t n_design, n_bins, nb;
+    double bin_s, max_rt;
+    double* params;
+    double* src_params;
+    double* avg_dir;
+    double* loudness;
+};
+
+template <int ORDER>
+__global__ void analyze_kernel(const AnalyzeParams P) {
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    __shared__ double s_B[kMaxDesign * NK];
+    __shared__ double s_g[kMaxBands][kMaxDesign];
+    __shared__ int s_first;
+    const int s = blockIdx.x;
+    const int b = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nb = P.nb;
+    const int nbins = P.n_bins;
+    if (threadIdx.x == 0) s_first = INT_MAX;
+    for (int j = threadIdx.x; j < P.n_design; j += blockDim.x) {
+        double Y[NK];
+        eval_sh<ORDER>(P.design[3 * j], P.design[3 * j + 1], P.design[3 * j + 2], Y);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) s_B[j * NK + k] = Y[k];
+    }
+    __syncthreads();
+
+    const float* Hs = P.H + (size_t)s * nbins * nb * NK + b * NK;
+    const size_t stride = (size_t)nb * NK;
+
+    // ---- pass 1: support of I_b(t) = H[t,b,0] / Y00 and directivity sums
+    int last = -1, first = INT_MAX, nnz = 0;
+    double S[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) S[k] = 0.0;
+    for (int t = lane; t < nbins; t += 32) {
+        const float* row = Hs + t * stride;
+        const double I = (double)row[0] / kY00;
+        if (I > 0.0) {
+            last = max(last, t);
+            first = min(first, t);
+            ++nnz;
+        }
+#pragma unroll
+        for (int k = 0; k < NK; ++k) S[k] += (double)row[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        last = max(last, __shfl_xor_sync(kAll, last, o));
+        first = min(first, __shfl_xor_sync(kAll, first, o));
+        nnz += __shfl_xor_sync(kAll, nnz, o);
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) S[k] = warp_sum(S[k]);
+    const double total = S[0] / kY00;
+
+    // ---- pass 2: Schroeder backward integration from the last non-zero bin
+    // (truncation) and least-squares fits on [-35,-5] / [-25,-5] dB
+    double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
+    double db_last = 0.0;
+    if (nnz >= 3) {
+        const int len = last + 1;
+        const int chunk = (len + 31) / 32;
+        const int lo = min(lane * chunk, len), hi = min(lo + chunk, len);
+        double csum = 0.0;
+        for (int t = hi - 1; t >= lo; --t) csum += (double)Hs[t * stride] / kY00;
+        // inclusive suffix scan over lanes (lane l: sum of chunks l..31)
+        double suf = csum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double v = __shfl_down_sync(kAll, suf, o);
+            if (lane + o < 32) suf += v;
+        }
+        const double edc0 = __shfl_sync(kAll, suf, 0);
+        double acc = suf - csum;   // energy after this lane's chunk
+        for (int t = hi - 1; t >= lo; --t) {
+            acc += (double)Hs[t * stride] / kY00;
+            const double db = 10.0 * log10(acc / edc0);
+            const double x = (double)t * P.bin_s;
+            if (t == last) db_last = db;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const double lim = r == 0 ? -35.0 : -25.0;
+                if (db <= -5.0 && db >= lim) {
+                    fit[r][0] += 1.0;
+                    fit[r][1] += x;
+                    fit[r][2] += db;
+                    fit[r][3] += x * db;
+                    fit[r][4] += x * x;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) fit[r][i] = warp_sum(fit[r][i]);
+        db_last = warp_sum(db_last);   // only the owner of `last` contributes
+    }
+
+    // ---- per-band outputs (lane 0 writes)
+    bool silent = nnz < 3;
+    double slope = 0.0, nfit = 0.0;
+    if (!silent) {
+        const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
+        if (r < 0) {
+            silent = true;
+        } else {
+            const double n = fit[r][0], sx = fit[r][1], sy = fit[r][2], sxy = fit[r][3], sxx = fit[r][4];
+            const double den = n * sxx - sx * sx;
+            if (n < 2.0 || !(den > 0.0)) {
+                silent = true;
+            } else {
+                slope = (n * sxy - sx * sy) / den;
+                nfit = n;
+                if (!(slope < 0.0)) silent = true;
+            }
+        }
+    }
+    double rt60 = 1.0;   // cold-start value for silent bands
+    if (!silent) rt60 = fmin(fmax(-60.0 / slope, 0.05), P.max_rt);
+    const double gain = (!silent && total > 0.0) ? sqrt(total / (rt60 / (6.0 * log(10.0)))) : 0.0;
+    const double edir = (double)P.Dir[((size_t)s * nb + b) * NK] / kY00;
+    double drr;
+    if (!(edir > 0.0)) drr = -99.0;
+    else if (!(total > 0.0)) drr = 99.0;
+    else drr = fmin(fmax(10.0 * log10(edir / total), -99.0), 99.0);
+    if (lane == 0) {
+        double* p = P.params + ((size_t)s * nb + b) * EF_P_COUNT;
+        p[EF_P_RT60] = rt60;
+        p[EF_P_GAIN] = gain;
+        p[EF_P_DRR_DB] = drr;
+        p[EF_P_TOTAL] = total;
+        p[EF_P_DIRECT] = edir;
+        p[EF_P_SILENT] = silent ? 1.0 : 0.0;
+        p[EF_P_FIT_N] = nfit;
+        p[EF_P_SLOPE] = slope;
+        if (first != INT_MAX) atomicMin(&s_first, first);
+    }
+
+    // ---- average directivity and loudness (sh.py:240-253)
+    double avg[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) avg[k] = total > 0.0 ? S[k] / total : 0.0;
+    if (lane == 0 && P.avg_dir) {
+        double* a = P.avg_dir + ((size_t)s * nb + b) * NK;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) a[k] = avg[k];
+    }
+    if (P.loudness) {
+        for (int j = lane; j < P.n_design; j += 32) {
+            double g = 0.0;
+#pragma unroll
+            for (int k = 0; k < NK; ++k) g += s_B[j * NK + k] * avg[k];
+            s_g[b][j] = fmax(0.0, g);
+        }
+        __syncwarp();
+        const double scale = 4.0 * M_PI / (double)P.n_design;
+        double* D = P.loudness + ((size_t)s * nb + b) * NK * NK;
+        for (int e = lane; e < NK * NK; e += 32) {
+            const int k1 = e / NK, k2 = e % NK;
+            double acc = 0.0;
+            for (int j = 0; j < P.n_design; ++j) acc += s_B[j * NK + k1] * s_g[b][j] * s_B[j * NK + k2];
+            D[e] = scale * acc;
+        }
+    }
+    // ---- per-source outputs
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double* q = P.src_params + (size_t)s * EF_S_COUNT;
+        q[EF_S_PREDELAY] = s_first == INT_MAX ? -1.0 : (double)s_first * P.bin_s;
+        const unsigned long long nrefl = P.stats[(size_t)s * EF_ST_COUNT + EF_ST_REFLECTIONS];
+        q[EF_S_MFP] = nrefl ? P.sum_t[s] / (double)nrefl : 0.0;
+        q[EF_S_SILENT] = s_first == INT_MAX ? 1.0 : 0.0;
+        q[3] = 0.0;
+    }
+}
+
+__global__ void blend_kernel(const float* __restrict__ cache, const float* __restrict__ frame,
+                             int64_t n, float a, float b, float* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a * frame[i] + b * cache[i];
+}
+
+}  // namespace ef
+
+using namespace ef;
+
+extern "C" int ef_blend(const float* cache, const float* frame, int64_t n, double alpha, float* out,
+                        void* stream) {
+    if (n < 0 || !(alpha >= 0.0 && alpha <= 1.0)) return set_error(EF_EINVAL, "ef_blend: bad n or alpha");
+    if (n == 0) return EF_OK;
+    if (!cache || !frame || !out) return set_error(EF_EINVAL, "ef_blend: null argument");
+    const long long g = std::min<long long>((n + 255) / 256, 148LL * 16);
+    blend_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(cache, frame, n, (float)alpha,
+                                                           (float)(1.0 - alpha), out);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "blend_kernel");
+}
+
+extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const float* Dir,
+                          const unsigned long long* stats, const double* sum_t,
+                          const double* design, int32_t n_design, double* params,
+                          double* src_params, double* avg_dir, double* loudness, void* stream) {
+    if (!cfg || !H || !Dir || !stats || !sum_t || !params || !src_params)
+        return set_error(EF_EINVAL, "ef_analyze: null argument");
+    if (cfg->order < 0 || cfg->order > kMaxOrder) return set_error(EF_EINVAL, "ef_analyze: order must be in [0, 4]");
+    if (cfg->n_bands < 1 || cfg->n_bands > kMaxBands) return set_error(EF_EINVAL, "ef_analyze: n_bands must be in [1, 8]");
+    if (cfg->n_sources < 1 || cfg->n_bins < 1) return set_error(EF_EINVAL, "ef_analyze: empty histogram");
+    if (loudness && (!design || n_design < 1 || n_design > kMaxDesign))
+        return set_error(EF_EINVAL, "ef_analyze: loudness needs a t-design of 1..64 directions");
+    if (!(cfg->bin_s > 0.0) || !(cfg->max_rt >= 0.05)) return set_error(EF_EINVAL, "ef_analyze: bad bin_s / max_rt");
+    AnalyzeParams P{H, Dir, stats, sum_t, design, loudness ? n_design : 0, cfg->n_bins, cfg->n_bands,
+                    cfg->bin_s, cfg->max_rt, params, src_params, avg_dir, loudness};
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 grid(cfg->n_sources), block(32 * cfg->n_bands);
+    switch (cfg->order) {
+        case 0: analyze_kernel<0><<<grid, block, 0, st>>>(P); break;
+        case 1: analyze_kernel<1><<<grid, block, 0, st>>>(P); break;
+        case 2: analyze_kernel<2><<<grid, block, 0, st>>>(P); break;
+        case 3: analyze_kernel<3><<<grid, block, 0, st>>>(P); break;
+        default: analyze_kernel<4><<<grid, block, 0, st>>>(P); break;
+    }
+    count_launch();
+    return check_cuda(cudaGetLastError(), "analyze_kernel");
+}

@@ -1,0 +1,287 @@
+// Device-side building blocks of the hot path (compiled with -fmad=false:
+// every f64 expression below is evaluated exactly as written, matching the
+// reference's numpy evaluation order bit-for-bit).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ef_internal.h"
+
+namespace ef {
+
+// ---------------------------------------------------------------- RNG ----
+// Philox4x32-10 (Salmon et al. 2011); key = (seed, source key),
+// counter = (ray, bounce, draw, frame).  DESIGN.md 3.1.
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+    return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+
+__device__ __forceinline__ void draw2(uint32_t ray, uint32_t bounce, uint32_t draw, uint32_t frame,
+                                      uint32_t seed, uint32_t src, double& u1, double& u2) {
+    const uint4 x = philox(make_uint4(ray, bounce, draw, frame), make_uint2(seed, src));
+    u1 = u53(x.x, x.y);
+    u2 = u53(x.z, x.w);
+}
+
+// Uniform sphere direction, Marsaglia rejection.
+__device__ __forceinline__ void sample_sphere(uint32_t seed, uint32_t src, uint32_t ray,
+                                              uint32_t frame, double& dx, double& dy, double& dz) {
+    dx = 0.0; dy = 0.0; dz = 1.0;
+    for (uint32_t j = 0; j < 64u; ++j) {
+        double u1, u2;
+        draw2(ray, 0u, j, frame, seed, src, u1, u2);
+        const double a = 2.0 * u1 - 1.0;
+        const double b = 2.0 * u2 - 1.0;
+        const double s = a * a + b * b;
+        if (s >= 1.0) continue;
+        const double f = 2.0 * sqrt(1.0 - s);
+        dx = a * f;
+        dy = b * f;
+        dz = 1.0 - 2.0 * s;
+        break;
+    }
+}
+
+// Cosine lobe about unit n: disk rejection + Duff et al. ONB.
+__device__ __forceinline__ void sample_cosine(uint32_t seed, uint32_t src, uint32_t ray,
+                                              uint32_t bounce, uint32_t frame, double nx, double ny,
+                                              double nz, double& dx, double& dy, double& dz) {
+    dx = nx; dy = ny; dz = nz;
+    for (uint32_t j = 0; j < 64u; ++j) {
+        double u1, u2;
+        draw2(ray, bounce, 1u + j, frame, seed, src, u1, u2);
+        const double a = 2.0 * u1 - 1.0;
+        const double b = 2.0 * u2 - 1.0;
+        const double s = a * a + b * b;
+        if (s >= 1.0) continue;
+        const double z = sqrt(1.0 - s);
+        const double sg = copysign(1.0, nz);
+        const double aa = -1.0 / (sg + nz);
+        const double bb = nx * ny * aa;
+        const double t1x = 1.0 + sg * nx * nx * aa, t1y = sg * bb, t1z = -sg * nx;
+        const double t2x = bb, t2y = sg + ny * ny * aa, t2z = -ny;
+        dx = (a * t1x + b * t2x) + z * nx;
+        dy = (a * t1y + b * t2y) + z * ny;
+        dz = (a * t1z + b * t2z) + z * nz;
+        break;
+    }
+}
+
+// ------------------------------------------------------ exact geometry ----
+// np.einsum 3-term order (p0 + p2) + p1, no FMA.
+__device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1,
+                                       double b2) {
+    return (a0 * b0 + a2 * b2) + a1 * b1;
+}
+
+// Moeller-Trumbore exactly as bvh.py:17-27 / bvh.py:33-44.  Returns the
+// barycentric-valid flag (without the t window); writes t.
+__device__ __forceinline__ bool mt_exact(double ox, double oy, double oz, double dx, double dy,
+                                         double dz, const double* __restrict__ v, double& t) {
+    const double v0x = v[0], v0y = v[1], v0z = v[2];
+    const double e1x = v[3], e1y = v[4], e1z = v[5];
+    const double e2x = v[6], e2y = v[7], e2z = v[8];
+    // pvec = cross(d, e2)
+    const double px = dy * e2z - dz * e2y;
+    const double py = dz * e2x - dx * e2z;
+    const double pz = dx * e2y - dy * e2x;
+    const double det = dot3(e1x, e1y, e1z, px, py, pz);
+    if (!(fabs(det) > 1e-14)) return false;
+    const double inv = 1.0 / det;
+    const double tx = ox - v0x, ty = oy - v0y, tz = oz - v0z;
+    const double u = dot3(tx, ty, tz, px, py, pz) * inv;
+    if (!(u >= -1e-10)) return false;
+    // qvec = cross(tvec, e1)
+    const double qx = ty * e1z - tz * e1y;
+    const double qy = tz * e1x - tx * e1z;
+    const double qz = tx * e1y - ty * e1x;
+    const double vv = dot3(qx, qy, qz, dx, dy, dz) * inv;
+    if (!(vv >= -1e-10) || !(u + vv <= 1.0 + 1e-10)) return false;
+    t = dot3(e2x, e2y, e2z, qx, qy, qz) * inv;
+    return true;
+}
+
+// The full reference formula for one pair, including the values it yields
+// for invalid pairs (inv_det = 0 -> u = v = t = 0), bvh.py:17-27.
+__device__ __forceinline__ bool mt_full(double ox, double oy, double oz, double dx, double dy,
+                                        double dz, const double* __restrict__ v, double& t) {
+    const double v0x = v[0], v0y = v[1], v0z = v[2];
+    const double e1x = v[3], e1y = v[4], e1z = v[5];
+    const double e2x = v[6], e2y = v[7], e2z = v[8];
+    const double px = dy * e2z - dz * e2y;
+    const double py = dz * e2x - dx * e2z;
+    const double pz = dx * e2y - dy * e2x;
+    const double det = dot3(e1x, e1y, e1z, px, py, pz);
+    const bool ok = fabs(det) > 1e-14;
+    const double inv = ok ? 1.0 / det : 0.0;
+    const double tx = ox - v0x, ty = oy - v0y, tz = oz - v0z;
+    const double u = dot3(tx, ty, tz, px, py, pz) * inv;
+    const double qx = ty * e1z - tz * e1y;
+    const double qy = tz * e1x - tx * e1z;
+    const double qz = tx * e1y - ty * e1x;
+    const double vv = dot3(qx, qy, qz, dx, dy, dz) * inv;
+    t = dot3(e2x, e2y, e2z, qx, qy, qz) * inv;
+    return ok && (u >= -1e-10) && (vv >= -1e-10) && (u + vv <= 1.0 + 1e-10);
+}
+
+// ----------------------------------------------------------- traversal ----
+struct RayF {
+    float ox, oy, oz;    // origin * inv (for the FMA slab form)
+    float ix, iy, iz;    // 1 / direction
+};
+
+__device__ __forceinline__ float safe_inv(double d) {
+    float f = (float)d;
+    if (fabsf(f) < 1e-20f) f = copysignf(1e-20f, f);
+    return __frcp_rn(f);
+}
+
+__device__ __forceinline__ RayF make_rayf(double ox, double oy, double oz, double dx, double dy,
+                                          double dz) {
+    RayF r;
+    r.ix = safe_inv(dx);
+    r.iy = safe_inv(dy);
+    r.iz = safe_inv(dz);
+    r.ox = __fmul_rn((float)ox, r.ix);
+    r.oy = __fmul_rn((float)oy, r.iy);
+    r.oz = __fmul_rn((float)oz, r.iz);
+    return r;
+}
+
+// Conservative slab test of one f32 box; returns entry distance or +inf.
+__device__ __forceinline__ float slab(const RayF& r, float lox, float hix, float loy, float hiy,
+                                      float loz, float hiz, float tmin, float tmax) {
+    const float x0 = __fmaf_rn(lox, r.ix, -r.ox), x1 = __fmaf_rn(hix, r.ix, -r.ox);
+    const float y0 = __fmaf_rn(loy, r.iy, -r.oy), y1 = __fmaf_rn(hiy, r.iy, -r.oy);
+    const float z0 = __fmaf_rn(loz, r.iz, -r.oz), z1 = __fmaf_rn(hiz, r.iz, -r.oz);
+    const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));
+    const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));
+    return tn <= __fmul_rn(tf, 1.0000038f) ? tn : INFINITY;
+}
+
+struct Hit {
+    double t;
+    int32_t id;  // original triangle id, INT32_MAX = none
+};
+
+// Closest hit over the device BVH.  Accepts t in (t_min, t_max]; equal t
+// resolves to the lowest triangle id, so the answer is independent of the
+// tree and of the traversal order.
+__device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
+                                           const GpuTri* __restrict__ tris, double ox, double oy,
+                                           double oz, double dx, double dy, double dz, double t_min,
+                                           double t_max) {
+    Hit h{t_max, INT32_MAX};
+    const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
+    const float tminf = __double2float_rd(t_min);
+    float tb = __double2float_ru(t_max);
+    int32_t stack_node[kStackSize];
+    float stack_t[kStackSize];
+    int sp = 0;
+    int32_t node = 0;
+    for (;;) {
+        if (node >= 0) {
+            const float4* p = reinterpret_cast<const float4*>(nodes + node);
+            const float4 a = __ldg(p + 0), b = __ldg(p + 1), c = __ldg(p + 2);
+            const int4 d = __ldg(reinterpret_cast<const int4*>(p + 3));
+            const float t0 = slab(r, a.x, a.y, a.z, a.w, c.x, c.y, tminf, tb);
+            const float t1 = slab(r, b.x, b.y, b.z, b.w, c.z, c.w, tminf, tb);
+            const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
+            if (h0 && h1) {
+                const bool first0 = t0 <= t1;
+                stack_node[sp] = first0 ? d.y : d.x;
+                stack_t[sp] = first0 ? t1 : t0;
+                ++sp;
+                node = first0 ? d.x : d.y;
+                continue;
+            }
+            if (h0 || h1) {
+                node = h0 ? d.x : d.y;
+                continue;
+            }
+        } else {
+            const uint32_t enc = ~(uint32_t)node;
+            const uint32_t start = enc >> 3, cnt = (enc & 7u) + 1u;
+            for (uint32_t i = 0; i < cnt; ++i) {
+                const GpuTri* tp = tris + start + i;
+                double v[9];
+                const double2* q = reinterpret_cast<const double2*>(tp);
+                const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2),
+                              q3 = __ldg(q + 3), q4 = __ldg(q + 4);
+                v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y; v[4] = q2.x;
+                v[5] = q2.y; v[6] = q3.x; v[7] = q3.y; v[8] = q4.x;
+                const int32_t id = (int32_t)__double_as_longlong(q4.y);
+                double t;
+                if (mt_exact(ox, oy, oz, dx, dy, dz, v, t) && t > t_min && t <= h.t &&
+                    (t < h.t || id < h.id)) {
+                    h.t = t;
+                    h.id = id;
+                    tb = __double2float_ru(t);
+                }
+            }
+        }
+        // pop the next node still in front of the current closest hit
+        for (;;) {
+            if (sp == 0) return h;
+            --sp;
+            if (stack_t[sp] <= tb) break;
+        }
+        node = stack_node[sp];
+    }
+}
+
+// ------------------------------------------------------------------ SH ----
+// Real SH, ACN order, exactly sh.py:94-125 (same expression trees).
+template <int ORDER>
+__device__ __forceinline__ void eval_sh(double x, double y, double z, double* out) {
+    constexpr double C0 = 0.28209479177387814;
+    constexpr double C1 = 0.4886025119029199;
+    out[0] = C0;
+    if (ORDER >= 1) {
+        out[1] = -C1 * y;
+        out[2] = C1 * z;
+        out[3] = -C1 * x;
+    }
+    if (ORDER >= 2) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        out[4] = 1.0925484305920792 * x * y;
+        out[5] = -1.0925484305920792 * y * z;
+        out[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+        out[7] = -1.0925484305920792 * x * z;
+        out[8] = 0.5462742152960396 * (xx - yy);
+        if (ORDER >= 3) {
+            out[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+            out[10] = 2.890611442640554 * x * y * z;
+            out[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+            out[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            out[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+            out[14] = 1.445305721320277 * z * (xx - yy);
+            out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+        }
+        if (ORDER >= 4) {
+            out[16] = 2.5033429417967046 * x * y * (xx - yy);
+            out[17] = -1.7701307697799304 * y * z * (3.0 * xx - yy);
+            out[18] = 0.9461746957575601 * x * y * (7.0 * zz - 1.0);
+            out[19] = -0.6690465435572892 * y * z * (7.0 * zz - 3.0);
+            out[20] = 0.10578554691520431 * (zz * (35.0 * zz - 30.0) + 3.0);
+            out[21] = -0.6690465435572892 * x * z * (7.0 * zz - 3.0);
+            out[22] = 0.47308734787878004 * (xx - yy) * (7.0 * zz - 1.0);
+            out[23] = -1.7701307697799304 * x * z * (xx - 3.0 * yy);
+            out[24] = 0.6258357354491761 * (xx * (xx - 3.0 * yy) - yy * (3.0 * xx - yy));
+        }
+    }
+}
+
+}  // namespace ef

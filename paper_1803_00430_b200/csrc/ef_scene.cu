@@ -1,0 +1,158 @@
+// Scene construction: validates the reference's arrays, builds the device
+// BVH (bvh_build.cpp) and uploads everything once (SceneModel.__init__,
+// scene.py:149-171; SceneModel is immutable after construction).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ef_internal.h"
+
+using namespace ef;
+
+namespace {
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t count, int64_t& bytes) {
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc((void**)dst, count * sizeof(T));
+    if (e != cudaSuccess) return e;
+    bytes += (int64_t)(count * sizeof(T));
+    return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+void free_scene(ef_scene* s) {
+    if (!s) return;
+    cudaFree(s->nodes);
+    cudaFree(s->tris);
+    cudaFree(s->tris_by_id);
+    cudaFree(s->normals);
+    cudaFree(s->mat);
+    cudaFree(s->fd);
+    cudaFree(s->fs);
+    cudaFree(s->pdiff);
+    delete s;
+}
+
+}  // namespace
+
+extern "C" int ef_scene_create(const double* v0, const double* e1, const double* e2,
+                               const double* normals, const int64_t* material_index, int64_t n_tri,
+                               const double* absorption, const double* scattering,
+                               int32_t n_materials, int32_t n_bands, ef_scene** out) {
+    if (!out) return set_error(EF_EINVAL, "ef_scene_create: out is null");
+    *out = nullptr;
+    if (n_tri < 0) return set_error(EF_EINVAL, "ef_scene_create: n_tri < 0");
+    if (n_bands < 1 || n_bands > kMaxBands)
+        return set_error(EF_EINVAL, "ef_scene_create: n_bands must be in [1, 8]");
+    if (n_materials < 1) return set_error(EF_EINVAL, "ef_scene_create: need at least one material");
+    if (!absorption || !scattering) return set_error(EF_EINVAL, "ef_scene_create: null material table");
+    if (n_tri > 0 && (!v0 || !e1 || !e2 || !normals || !material_index))
+        return set_error(EF_EINVAL, "ef_scene_create: null geometry array");
+    for (int64_t i = 0; i < (int64_t)n_materials * n_bands; ++i) {
+        // Material.__post_init__ (scene.py:38-45)
+        if (!(absorption[i] >= 0.0 && absorption[i] <= 1.0) ||
+            !(scattering[i] >= 0.0 && scattering[i] <= 1.0))
+            return set_error(EF_EINVAL, "ef_scene_create: absorption and scattering coefficients must lie in [0, 1]");
+    }
+    for (int64_t t = 0; t < n_tri; ++t)
+        if (material_index[t] < 0 || material_index[t] >= n_materials)
+            return set_error(EF_EINVAL, "ef_scene_create: material index out of range at triangle " + std::to_string(t));
+    for (int64_t i = 0; i < 9 * n_tri / 3; ++i)
+        if (!std::isfinite(v0[i]) || !std::isfinite(e1[i]) || !std::isfinite(e2[i]))
+            return set_error(EF_EINVAL, "ef_scene_create: non-finite vertex data");
+
+    ef_scene* s = new ef_scene();
+    s->n_tri = n_tri;
+    s->n_bands = n_bands;
+    s->n_mat = n_materials;
+    try {
+        // material reflection factors: p = mean_b(s_b) summed
+        // sequentially; E_b *= (1 - a_b) * s_b/p (diffuse) or (1-s_b)/(1-p)
+        std::vector<float> fd((size_t)n_materials * n_bands), fs(fd.size());
+        std::vector<double> pd(n_materials);
+        for (int m = 0; m < n_materials; ++m) {
+            double p = 0.0;
+            for (int b = 0; b < n_bands; ++b) p += scattering[m * n_bands + b];
+            p = p / (double)n_bands;
+            pd[m] = p;
+            for (int b = 0; b < n_bands; ++b) {
+                const double keep = 1.0 - absorption[m * n_bands + b];
+                const double sb = scattering[m * n_bands + b];
+                fd[m * n_bands + b] = p > 0.0 ? (float)(keep * (sb / p)) : 0.0f;
+                fs[m * n_bands + b] = p < 1.0 ? (float)(keep * ((1.0 - sb) / (1.0 - p))) : 0.0f;
+            }
+        }
+        cudaError_t e = cudaSuccess;
+#define EF_UP(dst, src, n)                                                        \
+    if (e == cudaSuccess) e = upload(&s->dst, src, n, s->device_bytes);
+        EF_UP(fd, fd.data(), fd.size());
+        EF_UP(fs, fs.data(), fs.size());
+        EF_UP(pdiff, pd.data(), pd.size());
+        if (n_tri > 0) {
+            HostBvh bvh;
+            build_bvh(v0, e1, e2, n_tri, bvh);
+            std::vector<GpuTri> tris(n_tri);
+            std::vector<double> by_id(9 * n_tri);
+            std::vector<int32_t> mat(n_tri);
+            for (int64_t i = 0; i < n_tri; ++i) {
+                const int64_t id = bvh.order[i];
+                for (int k = 0; k < 3; ++k) {
+                    tris[i].v[k] = v0[3 * id + k];
+                    tris[i].v[3 + k] = e1[3 * id + k];
+                    tris[i].v[6 + k] = e2[3 * id + k];
+                }
+                tris[i].id = id;
+            }
+            for (int64_t t = 0; t < n_tri; ++t) {
+                for (int k = 0; k < 3; ++k) {
+                    by_id[9 * t + k] = v0[3 * t + k];
+                    by_id[9 * t + 3 + k] = e1[3 * t + k];
+                    by_id[9 * t + 6 + k] = e2[3 * t + k];
+                }
+                mat[t] = (int32_t)material_index[t];
+            }
+            s->n_nodes = (int64_t)bvh.nodes.size();
+            s->max_depth = bvh.max_depth;
+            s->max_leaf = bvh.max_leaf;
+            if (bvh.max_depth + 2 >= kStackSize) {
+                free_scene(s);
+                return set_error(EF_EUNSUPPORTED, "ef_scene_create: BVH deeper than the traversal stack");
+            }
+            EF_UP(nodes, bvh.nodes.data(), bvh.nodes.size());
+            EF_UP(tris, tris.data(), tris.size());
+            EF_UP(tris_by_id, by_id.data(), by_id.size());
+            EF_UP(normals, normals, (size_t)3 * n_tri);
+            EF_UP(mat, mat.data(), mat.size());
+        }
+#undef EF_UP
+        if (e != cudaSuccess) {
+            free_scene(s);
+            return check_cuda(e, "ef_scene_create upload");
+        }
+    } catch (const std::exception& ex) {
+        free_scene(s);
+        return set_error(EF_EINVAL, std::string("ef_scene_create: ") + ex.what());
+    }
+    *out = s;
+    return EF_OK;
+}
+
+extern "C" int ef_scene_destroy(ef_scene* s) {
+    free_scene(s);
+    return EF_OK;
+}
+
+extern "C" int ef_scene_info(const ef_scene* s, int64_t* o) {
+    if (!s || !o) return set_error(EF_EINVAL, "ef_scene_info: null argument");
+    o[0] = s->n_tri;
+    o[1] = s->n_nodes;
+    o[2] = s->max_depth;
+    o[3] = s->device_bytes;
+    o[4] = s->max_leaf;
+    o[5] = s->n_bands;
+    o[6] = s->n_mat;
+    return EF_OK;
+}

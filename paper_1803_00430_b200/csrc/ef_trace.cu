@@ -1,0 +1,585 @@
+// K1 + K3: counter-based ray generation and the persistent trace megakernel
+// (closest hit -> listener sphere -> SH histogram commit -> reflection), plus
+// the batched ray-query and SH kernels behind the reference's query API.
+//
+// Reference functions replaced (see include/echoforge_b200.h):
+//   SceneModel.intersect_batch  scene.py:208-230
+//   BVH.intersect               bvh.py:130-160
+//   SceneModel.occluded_batch   scene.py:232-252
+//   eval_sh_batch               sh.py:86-126
+//   trace_frame                 SPEC.md:207-215 (bounce model: DESIGN.md 3)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+
+#include "ef_device.cuh"
+
+namespace ef {
+
+constexpr int kTraceThreads = 128;
+constexpr int kMaxSourcesPerLaunch = 256;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// all-pairs closest hit over triangles staged in shared memory (T <= 512),
+// ids ascending with a strict '<': ties go to the lowest id (scene.py:220)
+__device__ __forceinline__ Hit closest_brute(const double* __restrict__ s_tri, int n, double ox,
+                                             double oy, double oz, double dx, double dy, double dz,
+                                             double t_min, double t_max) {
+    Hit h{INFINITY, INT32_MAX};
+    for (int i = 0; i < n; ++i) {
+        double t;
+        if (mt_exact(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t) && t > t_min && t <= t_max &&
+            t < h.t) {
+            h.t = t;
+            h.id = i;
+        }
+    }
+    return h;
+}
+
+struct TraceParams {
+    const GpuNode* nodes;
+    const GpuTri* tris;
+    const double* tris_by_id;
+    int32_t n_tri;
+    const double* normals;
+    const int32_t* mat;
+    const float* fd;
+    const float* fs;
+    const double* pdiff;
+    int32_t nb;
+    const double* src_pos;
+    const uint32_t* src_key;
+    const uint32_t* ray_ids;
+    int32_t n_src;
+    int64_t n_rays;
+    uint32_t ray0, seed, frame;
+    int32_t n_bins, max_bounces;
+    double bin_len, lx, ly, lz, r2;
+    float e0;
+    float* H;
+    float* Dir;
+    unsigned long long* stats;
+    double* sum_t;
+    int32_t* path_nseg;
+    int32_t* path_ids;
+    unsigned long long* counter;
+    unsigned long long total;
+};
+
+struct LaneStats {
+    int src = -1;
+    uint32_t c[EF_ST_COUNT] = {};
+    double sum_t = 0.0;
+};
+
+__device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned long long* s_stats,
+                                            double* s_sumt) {
+    if (ls.src >= 0) {
+#pragma unroll
+        for (int i = 0; i < EF_ST_COUNT; ++i)
+            if (ls.c[i]) atomicAdd(&s_stats[ls.src * EF_ST_COUNT + i], (unsigned long long)ls.c[i]);
+        if (ls.sum_t != 0.0) atomicAdd(&s_sumt[ls.src], ls.sum_t);
+    }
+#pragma unroll
+    for (int i = 0; i < EF_ST_COUNT; ++i) ls.c[i] = 0;
+    ls.sum_t = 0.0;
+}
+
+template <int NBMAX, int ORDER, bool BRUTE>
+__global__ void __launch_bounds__(kTraceThreads) trace_kernel(const TraceParams P) {
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* s_stats = reinterpret_cast<unsigned long long*>(smem);
+    double* s_sumt = reinterpret_cast<double*>(s_stats + P.n_src * EF_ST_COUNT);
+    double* s_tri = s_sumt + P.n_src;
+    for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0ull;
+    for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
+    if (BRUTE)
+        for (int i = threadIdx.x; i < 9 * P.n_tri; i += blockDim.x) s_tri[i] = P.tris_by_id[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int nb = P.nb;
+    LaneStats ls;
+    bool active = false, exhausted = false;
+    double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 1, plen = 0;
+    float E[NBMAX];
+#pragma unroll
+    for (int b = 0; b < NBMAX; ++b) E[b] = 0.f;
+    uint32_t ray = 0, skey = 0;
+    int src = 0, nrefl = 0, nseg = 0;
+    unsigned long long path = 0;
+
+    for (;;) {
+        // ---- warp-aggregated refill: idle lanes take the next path indices
+        const bool need = !active && !exhausted;
+        const unsigned mask = __ballot_sync(kFull, need);
+        if (mask) {
+            const int leader = __ffs(mask) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(P.counter, (unsigned long long)__popc(mask));
+            base = __shfl_sync(kFull, base, leader);
+            if (need) {
+                path = base + __popc(mask & ((1u << lane) - 1u));
+                if (path >= P.total) {
+                    exhausted = true;
+                } else {
+                    src = (int)(path / (unsigned long long)P.n_rays);
+                    const int64_t local = (int64_t)(path - (unsigned long long)src * P.n_rays);
+                    ray = P.ray_ids ? __ldg(P.ray_ids + local) : P.ray0 + (uint32_t)local;
+                    skey = P.src_key ? __ldg(P.src_key + src) : (uint32_t)src;
+                    ox = __ldg(P.src_pos + 3 * src + 0);
+                    oy = __ldg(P.src_pos + 3 * src + 1);
+                    oz = __ldg(P.src_pos + 3 * src + 2);
+                    sample_sphere(P.seed, skey, ray, P.frame, dx, dy, dz);
+#pragma unroll
+                    for (int b = 0; b < NBMAX; ++b) E[b] = P.e0;
+                    plen = 0.0;
+                    nrefl = 0;
+                    nseg = 0;
+                    if (src != ls.src) {
+                        flush_stats(ls, s_stats, s_sumt);
+                        ls.src = src;
+                    }
+                    ls.c[EF_ST_PATHS]++;
+                    active = true;
+                }
+            }
+        }
+        if (__all_sync(kFull, !active)) break;
+        if (!active) continue;
+
+        // ---- closest hit (exact f64 leaf test)
+        Hit h;
+        if (BRUTE)
+            h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+        else
+            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+        const bool hit = h.id != INT32_MAX;
+        if (P.path_ids) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
+
+        // ---- listener sphere receiver + SH histogram commit
+        {
+            const double Lx = P.lx - ox, Ly = P.ly - oy, Lz = P.lz - oz;
+            const double tc = dot3(Lx, Ly, Lz, dx, dy, dz);
+            const double tlim = hit ? h.t : INFINITY;
+            if (tc > 0.0 && tc < tlim) {
+                const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
+                const double perp2 = dist2 - tc * tc;
+                if (perp2 <= P.r2) {
+                    float* dst = nullptr;
+                    ls.c[EF_ST_ARRIVALS]++;
+                    if (nrefl == 0) {
+                        ls.c[EF_ST_DIRECT]++;
+                        dst = P.Dir + (size_t)src * nb * NK;
+                    } else {
+                        const double q = (plen + tc) / P.bin_len;
+                        if (q < (double)P.n_bins)
+                            dst = P.H + ((size_t)src * P.n_bins + (size_t)q) * nb * NK;
+                        else
+                            ls.c[EF_ST_DROPPED]++;
+                    }
+                    if (dst) {
+                        double Y[NK];
+                        eval_sh<ORDER>(-dx, -dy, -dz, Y);
+                        float Yf[NK];
+#pragma unroll
+                        for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
+#pragma unroll
+                        for (int b = 0; b < NBMAX; ++b) {
+                            if (b < nb) {
+#pragma unroll
+                                for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, E[b] * Yf[k]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        ++nseg;
+        ls.c[EF_ST_SEGMENTS]++;
+        if (!hit) {
+            ls.c[EF_ST_ESCAPED]++;
+            active = false;
+        } else {
+            // ---- reflection
+            const double t = h.t;
+            plen += t;
+            ls.sum_t += t;
+            ox = ox + t * dx;
+            oy = oy + t * dy;
+            oz = oz + t * dz;
+            ++nrefl;
+            ls.c[EF_ST_REFLECTIONS]++;
+            const int m = __ldg(P.mat + h.id);
+            const double nx = __ldg(P.normals + 3 * h.id + 0);
+            const double ny = __ldg(P.normals + 3 * h.id + 1);
+            const double nz = __ldg(P.normals + 3 * h.id + 2);
+            double u1, u2;
+            draw2(ray, (uint32_t)nrefl, 0u, P.frame, P.seed, skey, u1, u2);
+            const bool diffuse = u1 < __ldg(P.pdiff + m);
+            const float* f = (diffuse ? P.fd : P.fs) + m * nb;
+#pragma unroll
+            for (int b = 0; b < NBMAX; ++b)
+                if (b < nb) E[b] = E[b] * __ldg(f + b);
+            const double nd = dot3(nx, ny, nz, dx, dy, dz);
+            if (diffuse) {
+                const double s = nd > 0.0 ? -1.0 : 1.0;
+                sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny, s * nz,
+                              dx, dy, dz);
+            } else {
+                const double k2 = 2.0 * nd;
+                dx = dx - k2 * nx;
+                dy = dy - k2 * ny;
+                dz = dz - k2 * nz;
+            }
+            if (nrefl >= P.max_bounces) active = false;
+        }
+        if (!active && P.path_nseg) P.path_nseg[path] = nseg;
+    }
+    flush_stats(ls, s_stats, s_sumt);
+    __syncthreads();
+    for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x)
+        if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
+    for (int i = threadIdx.x; i < P.n_src; i += blockDim.x)
+        if (s_sumt[i] != 0.0) atomicAdd(P.sum_t + i, s_sumt[i]);
+}
+
+// ---------------------------------------------------------------------------
+template <int NBMAX, int ORDER, bool BRUTE>
+static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
+    size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 8 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0);
+    auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTraceThreads, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, 1);
+    // persistent grid: every SM fully occupied, no more warps than paths
+    long long want = (long long)sms * per_sm;
+    long long need = ((long long)P.total + kTraceThreads - 1) / kTraceThreads;
+    int grid = (int)std::max(1LL, std::min(want, need));
+    kern<<<grid, kTraceThreads, smem, st>>>(P);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int NBMAX, bool BRUTE>
+static cudaError_t dispatch_order(int order, const TraceParams& P, cudaStream_t st) {
+    switch (order) {
+        case 0: return launch_trace<NBMAX, 0, BRUTE>(P, st);
+        case 1: return launch_trace<NBMAX, 1, BRUTE>(P, st);
+        case 2: return launch_trace<NBMAX, 2, BRUTE>(P, st);
+        case 3: return launch_trace<NBMAX, 3, BRUTE>(P, st);
+        default: return launch_trace<NBMAX, 4, BRUTE>(P, st);
+    }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void intersect_kernel(const GpuNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
+                                 const double* __restrict__ tris_by_id, int32_t n_tri, bool brute,
+                                 const double* __restrict__ o, const double* __restrict__ d,
+                                 int64_t n, double t_min, const double* __restrict__ t_max,
+                                 double* t_out, int64_t* tri_out, uint8_t* hit_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double ox = o[3 * i], oy = o[3 * i + 1], oz = o[3 * i + 2];
+        const double dx = d[3 * i], dy = d[3 * i + 1], dz = d[3 * i + 2];
+        const double tm = t_max ? t_max[i] : INFINITY;
+        Hit h;
+        if (brute)
+            h = closest_brute(tris_by_id, n_tri, ox, oy, oz, dx, dy, dz, t_min, tm);
+        else
+            h = closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, tm);
+        const bool hit = h.id != INT32_MAX;
+        t_out[i] = hit ? h.t : INFINITY;
+        tri_out[i] = hit ? h.id : -1;
+        hit_out[i] = hit;
+    }
+}
+
+// occluded_batch (scene.py:232-252): segment visibility with the
+// reference's limit = dist - RAY_EPS; all-pairs uses t < limit (scene.py:247),
+// the BVH path t <= limit (scene.py:250).
+__global__ void occluded_kernel(const GpuNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
+                                const double* __restrict__ tris_by_id, int32_t n_tri, bool brute,
+                                const double* __restrict__ o, const double* __restrict__ tg,
+                                int64_t n, uint8_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double ox = o[3 * i], oy = o[3 * i + 1], oz = o[3 * i + 2];
+        const double ex = tg[3 * i] - ox, ey = tg[3 * i + 1] - oy, ez = tg[3 * i + 2] - oz;
+        const double dist = sqrt((ex * ex + ey * ey) + ez * ez);   // np.linalg.norm order
+        const double safe = fmax(dist, 1e-12);
+        const double dx = ex / safe, dy = ey / safe, dz = ez / safe;
+        const double limit = dist - kRayEps;
+        bool blocked = false;
+        if (brute) {
+            for (int k = 0; k < n_tri && !blocked; ++k) {
+                double t;
+                blocked = mt_exact(ox, oy, oz, dx, dy, dz, tris_by_id + 9 * k, t) && t > kRayEps &&
+                          t < limit;
+            }
+        } else {
+            blocked = closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, kRayEps, limit).id != INT32_MAX;
+        }
+        out[i] = blocked;
+    }
+}
+
+template <int ORDER>
+__global__ void eval_sh_kernel(const double* __restrict__ dirs, int64_t n, double* __restrict__ out) {
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double Y[NK];
+        eval_sh<ORDER>(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], Y);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) out[i * NK + k] = Y[k];
+    }
+}
+
+__global__ void ray_triangles_kernel(const double* __restrict__ o, const double* __restrict__ d,
+                                     int64_t nr, const double* __restrict__ v0,
+                                     const double* __restrict__ e1, const double* __restrict__ e2,
+                                     int64_t nt, double t_min, const double* __restrict__ t_max,
+                                     double* t_out, uint8_t* valid_out) {
+    const int64_t total = nr * nt;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / nt, k = i - r * nt;
+        double v[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            v[c] = v0[3 * k + c];
+            v[3 + c] = e1[3 * k + c];
+            v[6 + c] = e2[3 * k + c];
+        }
+        double t;
+        bool ok = mt_full(o[3 * r], o[3 * r + 1], o[3 * r + 2], d[3 * r], d[3 * r + 1], d[3 * r + 2], v, t);
+        ok = ok && t > t_min && (!t_max || t <= t_max[r]);
+        t_out[i] = t;
+        valid_out[i] = ok;
+    }
+}
+
+template <int ORDER>
+__global__ void loudness_kernel(const double* __restrict__ avg, int64_t n,
+                                const double* __restrict__ design, int n_design, double* out) {
+    // one warp per distribution: gains on the design, then (4 pi/N) B^T diag(g) B
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    extern __shared__ double sh[];
+    double* sB = sh;                                       // n_design * NK
+    double* sg = sh + n_design * NK + (threadIdx.x >> 5) * n_design;
+    for (int j = threadIdx.x; j < n_design; j += blockDim.x) {
+        double Y[NK];
+        eval_sh<ORDER>(design[3 * j], design[3 * j + 1], design[3 * j + 2], Y);
+        for (int k = 0; k < NK; ++k) sB[j * NK + k] = Y[k];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= n) return;
+    const double* a = avg + w * NK;
+    for (int j = lane; j < n_design; j += 32) {
+        double g = 0.0;
+        for (int k = 0; k < NK; ++k) g += sB[j * NK + k] * a[k];
+        sg[j] = fmax(0.0, g);
+    }
+    __syncwarp();
+    const double scale = 4.0 * M_PI / (double)n_design;
+    for (int e = lane; e < NK * NK; e += 32) {
+        const int k1 = e / NK, k2 = e % NK;
+        double acc = 0.0;
+        for (int j = 0; j < n_design; ++j) acc += sB[j * NK + k1] * sg[j] * sB[j * NK + k2];
+        out[w * NK * NK + e] = scale * acc;
+    }
+}
+
+static int grid_for(int64_t n, int threads) {
+    long long g = (n + threads - 1) / threads;
+    return (int)std::max(1LL, std::min(g, 148LL * 32));
+}
+
+}  // namespace ef
+
+using namespace ef;
+
+extern "C" int ef_intersect_batch(const ef_scene* s, const double* origins, const double* dirs,
+                                  int64_t n, double t_min, const double* t_max, int32_t mode,
+                                  double* t_out, int64_t* tri_out, uint8_t* hit_out, void* stream) {
+    if (!s || (n > 0 && (!origins || !dirs || !t_out || !tri_out || !hit_out)))
+        return set_error(EF_EINVAL, "ef_intersect_batch: null argument");
+    if (mode < 0 || mode > 2) return set_error(EF_EINVAL, "ef_intersect_batch: mode must be 0, 1 or 2");
+    if (n == 0) return EF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (s->n_tri == 0) {
+        // scene.py:213-215: all miss
+        return set_error(EF_EUNSUPPORTED, "ef_intersect_batch: empty scene is handled by the host");
+    }
+    const bool brute = mode == 1 || (mode == 0 && s->n_tri <= kBruteMaxTris);
+    intersect_kernel<<<grid_for(n, 128), 128, 0, st>>>(s->nodes, s->tris, s->tris_by_id,
+                                                       (int32_t)s->n_tri, brute, origins, dirs, n,
+                                                       t_min, t_max, t_out, tri_out, hit_out);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "intersect_kernel");
+}
+
+extern "C" int ef_occluded_batch(const ef_scene* s, const double* origins, const double* targets,
+                                 int64_t n, uint8_t* out, void* stream) {
+    if (!s || (n > 0 && (!origins || !targets || !out)))
+        return set_error(EF_EINVAL, "ef_occluded_batch: null argument");
+    if (n == 0) return EF_OK;
+    if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_occluded_batch: empty scene is handled by the host");
+    const bool brute = s->n_tri <= kBruteMaxTris;
+    occluded_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+        s->nodes, s->tris, s->tris_by_id, (int32_t)s->n_tri, brute, origins, targets, n, out);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "occluded_kernel");
+}
+
+extern "C" int ef_eval_sh_batch(const double* dirs, int64_t n, int32_t order, double* out,
+                                void* stream) {
+    if (order < 0 || order > kMaxOrder)
+        return set_error(EF_EINVAL, "order must be in [0, 4], got " + std::to_string(order));
+    if (n == 0) return EF_OK;
+    if (!dirs || !out) return set_error(EF_EINVAL, "ef_eval_sh_batch: null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int g = grid_for(n, 128);
+    switch (order) {
+        case 0: eval_sh_kernel<0><<<g, 128, 0, st>>>(dirs, n, out); break;
+        case 1: eval_sh_kernel<1><<<g, 128, 0, st>>>(dirs, n, out); break;
+        case 2: eval_sh_kernel<2><<<g, 128, 0, st>>>(dirs, n, out); break;
+        case 3: eval_sh_kernel<3><<<g, 128, 0, st>>>(dirs, n, out); break;
+        default: eval_sh_kernel<4><<<g, 128, 0, st>>>(dirs, n, out); break;
+    }
+    count_launch();
+    return check_cuda(cudaGetLastError(), "eval_sh_kernel");
+}
+
+extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
+                        const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
+                        unsigned long long* stats, double* sum_t, int32_t* path_nseg,
+                        int32_t* path_ids, void* stream) {
+    if (!s || !cfg) return set_error(EF_EINVAL, "ef_trace: null scene or config");
+    if (cfg->n_sources < 1) return set_error(EF_EINVAL, "ef_trace: need at least one source");
+    if (cfg->order < 0 || cfg->order > kMaxOrder) return set_error(EF_EINVAL, "ef_trace: order must be in [0, 4]");
+    if (cfg->n_bins < 1 || cfg->max_bounces < 1 || cfg->n_rays < 1)
+        return set_error(EF_EINVAL, "ef_trace: n_bins, max_bounces and n_rays must be >= 1");
+    if (cfg->n_rays > 0xffffffffLL) return set_error(EF_EINVAL, "ef_trace: n_rays must fit in 32 bits");
+    if (!(cfg->bin_len > 0.0) || !(cfg->radius >= 0.0))
+        return set_error(EF_EINVAL, "ef_trace: bin_len must be > 0 and radius >= 0");
+    if (cfg->mode < 0 || cfg->mode > 2) return set_error(EF_EINVAL, "ef_trace: mode must be 0, 1 or 2");
+    if (!src_pos || !H || !Dir || !stats || !sum_t) return set_error(EF_EINVAL, "ef_trace: null buffer");
+    if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_trace: empty scene is handled by the host");
+    const bool brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= kBruteMaxTris);
+    if (brute && s->n_tri > 2048) return set_error(EF_EINVAL, "ef_trace: all-pairs mode supports <= 2048 triangles");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nk = (cfg->order + 1) * (cfg->order + 1);
+    cudaError_t e = cudaSuccess;
+    if (cfg->clear_outputs) {
+        // DMA-engine clears, no kernel launch
+        const size_t nh = (size_t)cfg->n_sources * cfg->n_bins * s->n_bands * nk;
+        e = cudaMemsetAsync(H, 0, nh * sizeof(float), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(Dir, 0, (size_t)cfg->n_sources * s->n_bands * nk * sizeof(float), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, (size_t)cfg->n_sources * EF_ST_COUNT * 8, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
+        if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
+    }
+    unsigned long long* counter = nullptr;
+    e = cudaMallocAsync((void**)&counter, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return check_cuda(e, "cudaMallocAsync");
+    for (int s0 = 0; s0 < cfg->n_sources; s0 += kMaxSourcesPerLaunch) {
+        const int ns = std::min(kMaxSourcesPerLaunch, cfg->n_sources - s0);
+        e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) break;
+        TraceParams P;
+        P.nodes = s->nodes;
+        P.tris = s->tris;
+        P.tris_by_id = s->tris_by_id;
+        P.n_tri = (int32_t)s->n_tri;
+        P.normals = s->normals;
+        P.mat = s->mat;
+        P.fd = s->fd;
+        P.fs = s->fs;
+        P.pdiff = s->pdiff;
+        P.nb = s->n_bands;
+        P.src_pos = src_pos + 3 * s0;
+        P.src_key = src_key ? src_key + s0 : nullptr;
+        P.ray_ids = ray_ids;
+        P.n_src = ns;
+        P.n_rays = cfg->n_rays;
+        P.ray0 = cfg->ray0;
+        P.seed = cfg->seed;
+        P.frame = cfg->frame;
+        P.n_bins = cfg->n_bins;
+        P.max_bounces = cfg->max_bounces;
+        P.bin_len = cfg->bin_len;
+        P.lx = cfg->listener[0];
+        P.ly = cfg->listener[1];
+        P.lz = cfg->listener[2];
+        P.r2 = cfg->radius * cfg->radius;
+        P.e0 = cfg->e0;
+        P.H = H + (size_t)s0 * cfg->n_bins * s->n_bands * nk;
+        P.Dir = Dir + (size_t)s0 * s->n_bands * nk;
+        P.stats = stats + (size_t)s0 * EF_ST_COUNT;
+        P.sum_t = sum_t + s0;
+        P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
+        P.path_ids = (path_ids && cfg->record_ids) ? path_ids + (size_t)s0 * cfg->n_rays * cfg->max_bounces : nullptr;
+        P.counter = counter;
+        P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
+        if (s->n_bands <= 4)
+            e = brute ? dispatch_order<4, true>(cfg->order, P, st) : dispatch_order<4, false>(cfg->order, P, st);
+        else
+            e = brute ? dispatch_order<8, true>(cfg->order, P, st) : dispatch_order<8, false>(cfg->order, P, st);
+        if (e != cudaSuccess) break;
+    }
+    cudaError_t e2 = cudaFreeAsync(counter, st);
+    if (e != cudaSuccess) return check_cuda(e, "trace_kernel");
+    return check_cuda(e2, "cudaFreeAsync");
+}
+
+extern "C" int ef_ray_triangles(const double* origins, const double* dirs, int64_t n_rays,
+                                const double* v0, const double* e1, const double* e2, int64_t n_tri,
+                                double t_min, const double* t_max, double* t_out, uint8_t* valid_out,
+                                void* stream) {
+    if (n_rays < 0 || n_tri < 0) return set_error(EF_EINVAL, "ef_ray_triangles: negative size");
+    if (n_rays == 0 || n_tri == 0) return EF_OK;
+    if (!origins || !dirs || !v0 || !e1 || !e2 || !t_out || !valid_out)
+        return set_error(EF_EINVAL, "ef_ray_triangles: null argument");
+    ray_triangles_kernel<<<grid_for(n_rays * n_tri, 128), 128, 0, (cudaStream_t)stream>>>(
+        origins, dirs, n_rays, v0, e1, e2, n_tri, t_min, t_max, t_out, valid_out);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "ray_triangles_kernel");
+}
+
+extern "C" int ef_loudness_batch(const double* avg, int64_t n, int32_t order, const double* design,
+                                 int32_t n_design, double* out, void* stream) {
+    if (order < 0 || order > kMaxOrder) return set_error(EF_EINVAL, "order must be in [0, 4]");
+    if (n == 0) return EF_OK;
+    if (!avg || !design || !out || n_design < 1 || n_design > 256)
+        return set_error(EF_EINVAL, "ef_loudness_batch: bad arguments");
+    const int nk = (order + 1) * (order + 1);
+    const int warps = 4;
+    const size_t smem = (size_t)(n_design * nk + warps * n_design) * sizeof(double);
+    const int grid = (int)((n + warps - 1) / warps);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (order) {
+        case 0: loudness_kernel<0><<<grid, 32 * warps, smem, st>>>(avg, n, design, n_design, out); break;
+        case 1: loudness_kernel<1><<<grid, 32 * warps, smem, st>>>(avg, n, design, n_design, out); break;
+        case 2: loudness_kernel<2><<<grid, 32 * warps, smem, st>>>(avg, n, design, n_design, out); break;
+        case 3: loudness_kernel<3><<<grid, 32 * warps, smem, st>>>(avg, n, design, n_design, out); break;
+        default: loudness_kernel<4><<<grid, 32 * warps, smem, st>>>(avg, n, design, n_design, out); break;
+    }
+    count_launch();
+    return check_cuda(cudaGetLastError(), "loudness_kernel");
+}

@@ -1,0 +1,243 @@
+"""Propagation -- trace_frame and friends, on the B200.
+
+The reference specifies this module but ships no code for it; the bounce
+model is pinned in DESIGN.md section 3 (forward tracing from point sources to
+a listener sphere, as BASELINE.json's configs require) and restated
+independently in oracle/efo.c, which the parity tests compare against.
+
+Hot path: one ``ef_trace`` launch traces every path of every source of a
+frame inside one persistent kernel (no return to the host per bounce), and
+commits arrivals straight into the device histogram
+H[source, bin, band, sh] (float32).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .sh import SH_C0, n_coeffs
+
+TAU_ER = 1.0
+TAU_LR = 3.0
+
+
+@dataclass
+class TraceConfig:
+    """Per-frame tracing parameters (SPEC RenderConfig subset, SPEC.md:589-592,
+    extended with the BASELINE configs' receiver and histogram shape)."""
+    primary_rays: int = 4096            # rays per source per frame
+    max_order: int = 50                 # reflections per path
+    sh_order: int = 2                   # histogram SH order (0..4)
+    bin_s: float = 1e-3                 # IR bin width, s
+    n_bins: int = 2000                  # IR length in bins
+    listener_radius: float = 0.5        # m
+    seed: int = 0
+    mode: int = 0                       # 0 reference dispatch, 1 all-pairs, 2 BVH
+    max_rt: float | None = None         # RT60 clamp (default: IR length)
+
+    @property
+    def n_coeffs(self) -> int:
+        return n_coeffs(self.sh_order)
+
+    def e0(self, total_rays: int | None = None) -> float:
+        """Initial per-band energy of a path: unit source power spread over
+        the rays and normalised by the receiver cross-section."""
+        n = self.primary_rays if total_rays is None else total_rays
+        return float(np.float32(1.0 / (n * math.pi * self.listener_radius ** 2)))
+
+
+@dataclass
+class LowRateIR:
+    """Energy IR with SH directivity.
+
+    ``histogram[t, b, k]`` = sum over arrivals in bin t of E_b * Y_k(arrival);
+    intensity = histogram[..., 0] / Y_00 and the directivity coefficients are
+    histogram / intensity.  ``direct[b, k]`` holds order-0 (unreflected)
+    arrivals.  Tensors stay on the device."""
+    sample_rate: float
+    histogram: object
+    direct: object
+
+    @property
+    def length(self) -> int:
+        return int(self.histogram.shape[0])
+
+    @property
+    def intensity(self):
+        return self.histogram[..., 0] / SH_C0
+
+    def numpy(self):
+        return self.histogram.detach().cpu().numpy(), self.direct.detach().cpu().numpy()
+
+
+@dataclass
+class TraceStats:
+    """SPEC.md:197-200 plus the receiver counters of DESIGN.md 3."""
+    mean_free_path: float
+    primary_rays_emitted: int
+    total_segments: int
+    reflections: int = 0
+    arrivals: int = 0
+    direct_arrivals: int = 0
+    dropped_late: int = 0
+    escaped: int = 0
+    open_field: bool = False
+
+
+@dataclass
+class PathList:
+    """Early-reflection paths.  ER extraction is the first
+    'next' item of SURVEY.md 8(f); this build routes all energy to the IR."""
+    delays: list = field(default_factory=list)
+    pressures: list = field(default_factory=list)
+    directivities: list = field(default_factory=list)
+    kinds: list = field(default_factory=list)
+
+
+@dataclass
+class CoherenceCaches:
+    """Temporal IR cache: exponentially smoothed histograms
+    per source key, updated by ``accumulate_ir``."""
+    tau_lr: float = TAU_LR
+    ir: dict = field(default_factory=dict)
+
+
+def _stats_from_row(row: np.ndarray, sum_t: float) -> TraceStats:
+    paths, segs, refl, arr, direct, dropped, esc = (int(x) for x in row[:7])
+    return TraceStats(mean_free_path=sum_t / refl if refl else 0.0,
+                      primary_rays_emitted=paths, total_segments=segs, reflections=refl,
+                      arrivals=arr, direct_arrivals=direct, dropped_late=dropped, escaped=esc,
+                      open_field=refl == 0)
+
+
+class FrameTracer:
+    """Device buffers + launches for repeated frames over a fixed scene and
+    source count: the batched form of ``trace_frame`` used by the bench and
+    the multi-source configs.  ``trace()`` is one ef_trace launch (plus a
+    histogram clear); nothing synchronises the host."""
+
+    def __init__(self, scene, n_sources: int, config: TraceConfig, record: bool = False):
+        t = _lib.torch()
+        dev = _lib.device()
+        self.scene = scene
+        self.config = config
+        self.n_sources = n_sources
+        self.nb = scene.n_bands
+        self.nk = config.n_coeffs
+        self.H = t.zeros((n_sources, config.n_bins, self.nb, self.nk), dtype=t.float32, device=dev)
+        self.Dir = t.zeros((n_sources, self.nb, self.nk), dtype=t.float32, device=dev)
+        self.stats = t.zeros((n_sources, _lib.EF_ST_COUNT), dtype=t.int64, device=dev)
+        self.sum_t = t.zeros((n_sources,), dtype=t.float64, device=dev)
+        self.src_pos = t.zeros((n_sources, 3), dtype=t.float64, device=dev)
+        self.src_key = t.arange(n_sources, dtype=t.int32, device=dev)
+        self.record = record
+        self.path_nseg = None
+        self.path_ids = None
+        self._handle = scene._device_handle()
+
+    def set_sources(self, positions, keys=None):
+        t = _lib.torch()
+        self.src_pos.copy_(t.as_tensor(np.asarray(positions, np.float64).reshape(-1, 3)))
+        if keys is not None:
+            self.src_key.copy_(t.as_tensor(np.asarray(keys, np.int64).astype(np.int32)))
+
+    def clear(self):
+        self.H.zero_()
+        self.Dir.zero_()
+        self.stats.zero_()
+        self.sum_t.zero_()
+
+    def trace(self, listener, frame: int = 0, ray0: int = 0, n_rays: int | None = None,
+              total_rays: int | None = None, ray_ids=None, clear: bool = True, stream=None):
+        """Launch ef_trace for all sources (rays [ray0, ray0+n_rays) of each,
+        or the explicit global indices ``ray_ids``)."""
+        t = _lib.torch()
+        c = self.config
+        ids = None
+        if ray_ids is not None:
+            ids = _lib.to_device(np.asarray(ray_ids, np.uint32).astype(np.int64), t.int64).to(t.int32)
+            n_rays = ids.shape[0]
+        n_rays = c.primary_rays if n_rays is None else int(n_rays)
+        cfg = _lib.TraceConfig()
+        cfg.n_sources = self.n_sources
+        cfg.order = c.sh_order
+        cfg.n_bins = c.n_bins
+        cfg.max_bounces = c.max_order
+        cfg.n_rays = n_rays
+        cfg.ray0 = ray0
+        cfg.seed = c.seed & 0xffffffff
+        cfg.frame = frame & 0xffffffff
+        cfg.mode = c.mode
+        cfg.bin_len = self.scene.speed_of_sound * c.bin_s
+        lp = np.asarray(listener, np.float64).reshape(3)
+        cfg.listener[:] = [float(x) for x in lp]
+        cfg.radius = c.listener_radius
+        cfg.e0 = c.e0(total_rays)
+        cfg.record_ids = int(self.record)
+        cfg.clear_outputs = int(bool(clear))
+        self.path_nseg = self.path_ids = None
+        if self.record:
+            self.path_nseg = t.zeros((self.n_sources, n_rays), dtype=t.int32, device=self.H.device)
+            self.path_ids = t.full((self.n_sources, n_rays, c.max_order), -2, dtype=t.int32,
+                                   device=self.H.device)
+        _lib.check(_lib.lib().ef_trace(
+            self._handle, cfg, _lib.ptr(self.src_pos), _lib.ptr(self.src_key), _lib.ptr(ids),
+            _lib.ptr(self.H), _lib.ptr(self.Dir), _lib.ptr(self.stats), _lib.ptr(self.sum_t),
+            _lib.ptr(self.path_nseg), _lib.ptr(self.path_ids), _lib.stream_handle(stream)))
+
+    def irs(self):
+        return [LowRateIR(1.0 / self.config.bin_s, self.H[s], self.Dir[s]) for s in range(self.n_sources)]
+
+    def trace_stats(self):
+        st = self.stats.cpu().numpy()
+        sm = self.sum_t.cpu().numpy()
+        return [_stats_from_row(st[s], float(sm[s])) for s in range(self.n_sources)]
+
+
+def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceCaches | None = None,
+                rng=None, frame: int = 0, dt: float | None = None):
+    """Trace one frame for one source.
+
+    ``rng``: an int seed (overrides config.seed) or None.  Returns
+    (PathList, LowRateIR, TraceStats).  With ``caches`` and ``dt`` the IR is
+    folded into the temporal cache (accumulate_ir) and the cached IR is
+    returned."""
+    if config.primary_rays < 1 or config.max_order < 1:
+        raise ValueError("config.primary_rays and config.max_order must be >= 1")
+    seed = config.seed if rng is None else int(rng)
+    cfg = TraceConfig(**{**config.__dict__, "seed": seed})
+    pos = source.pose_at(frame * (dt or 0.0)) if hasattr(source, "pose_at") else np.asarray(source)
+    lpos = listener.pose_at(frame * (dt or 0.0))[0] if hasattr(listener, "pose_at") else np.asarray(listener)
+    key = 0
+    if hasattr(scene, "sources") and source in scene.sources:
+        key = scene.sources.index(source)
+    if scene.n_triangles == 0:
+        t = _lib.torch()
+        dev = _lib.device()
+        ir = LowRateIR(1.0 / cfg.bin_s, t.zeros((cfg.n_bins, scene.n_bands, cfg.n_coeffs), device=dev),
+                       t.zeros((scene.n_bands, cfg.n_coeffs), device=dev))
+        return PathList(), ir, TraceStats(0.0, cfg.primary_rays, cfg.primary_rays, open_field=True)
+    tr = FrameTracer(scene, 1, cfg)
+    tr.set_sources(np.asarray(pos)[None, :], [key])
+    tr.trace(lpos, frame=frame)
+    ir = tr.irs()[0]
+    if caches is not None and dt is not None:
+        ir = accumulate_ir(caches.ir.get(key), ir, caches.tau_lr, dt)
+        caches.ir[key] = ir
+    return PathList(), ir, tr.trace_stats()[0]
+
+
+def accumulate_ir(cache_ir: LowRateIR | None, frame_ir: LowRateIR, tau: float, dt: float) -> LowRateIR:
+    """out = a*frame + (1-a)*cache, a = 1 - exp(-dt/tau)."""
+    if dt <= 0:
+        raise ValueError("dt must be > 0")
+    if cache_ir is None:
+        return frame_ir
+    a = 1.0 - math.exp(-dt / tau) if tau > 0 else 1.0
+    from .analysis import blend_histograms
+    return LowRateIR(frame_ir.sample_rate,
+                     blend_histograms(cache_ir.histogram, frame_ir.histogram, a),
+                     blend_histograms(cache_ir.direct, frame_ir.direct, a))
