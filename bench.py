@@ -110,10 +110,12 @@ def dist_env():
 
 
 # ----------------------------------------------------------------- CPU arm
-def cpu_oracle_rate(w, rays_per_source, threads):
+def cpu_oracle_rate(w, rays_per_source, threads, min_seconds=0.0):
     """CPU port of the reference algorithm (oracle/efo.c, reference BVH and
     traversal, the pinned bounce loop) on `threads` host threads: each thread
-    traces a contiguous ray shard of every source.  Returns (seg/s, segs, s)."""
+    traces a contiguous ray shard of every source; whole frames (frame index
+    0, 1, ...) repeat until `min_seconds` elapsed.  Returns (seg/s, segs, s,
+    frames)."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
@@ -126,17 +128,22 @@ def cpu_oracle_rate(w, rays_per_source, threads):
             shards.append((s, r0, min(per, rays_per_source - r0)))
 
     def run(job):
-        s, r0, n = job
+        s, r0, n, frame = job
         r = O.trace(os_, src_key=s, src_pos=w.sources[s], listener=w.listener, radius=w.radius,
-                    seed=w.seed, order=w.order, n_bins=w.n_bins, bin_len=bin_len,
+                    seed=w.seed, frame=frame, order=w.order, n_bins=w.n_bins, bin_len=bin_len,
                     max_bounces=w.max_bounces, e0=1.0, ray0=r0, n_rays=n)
         return r.stats["segments"]
 
+    segs, frames = 0, 0
     t0 = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
-        segs = sum(ex.map(run, shards))
+        while True:
+            segs += sum(ex.map(run, [j + (frames,) for j in shards]))
+            frames += 1
+            if time.perf_counter() - t0 >= min_seconds:
+                break
     dt = time.perf_counter() - t0
-    return segs / dt, segs, dt
+    return segs / dt, segs, dt, frames
 
 
 def run_reference(args, w, metric, unit):
@@ -145,11 +152,11 @@ def run_reference(args, w, metric, unit):
         return
     cores = len(os.sched_getaffinity(0))
     rays = max(1, int(w.n_rays * args.cpu_fraction))
-    for _ in range(args.warmup if args.warmup < 1 else 1):
+    for _ in range(min(args.warmup, 1)):
         cpu_oracle_rate(w, max(1, rays // 16), cores)
     rates, secs = [], []
     for _ in range(args.steps):
-        r, segs, dt = cpu_oracle_rate(w, rays, cores)
+        r, segs, dt, _ = cpu_oracle_rate(w, rays, cores)
         rates.append(r)
         secs.append(dt)
     value = float(np.median(rates))
@@ -317,10 +324,11 @@ def run_gpu(args, w, metric, unit):
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
         rays = max(1, int(w.n_rays * args.cpu_fraction))
-        rate, segs_c, dt = cpu_oracle_rate(w, rays, cores)
+        rate, segs_c, dt, frames = cpu_oracle_rate(w, rays, cores, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": unit, "cores": cores, "kind": "port",
-                                "sample": f"rays [0,{rays}) of each of the {len(w.sources)} sources "
-                                          f"({segs_c} segments, {dt:.2f} s)"}
+                                "sample": f"{frames} frames x rays [0,{rays}) of each of the "
+                                          f"{len(w.sources)} sources ({segs_c} segments, {dt:.1f} s, "
+                                          f"{cores} threads)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -329,13 +337,15 @@ def run_gpu(args, w, metric, unit):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(WORK))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-fraction", type=float, default=1.0,
                     help="fraction of each source's rays in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="minimum wall time of the CPU baseline sample")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1803_00430_b200 import workloads

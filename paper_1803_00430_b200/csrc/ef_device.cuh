@@ -182,7 +182,8 @@ struct Hit {
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
-                                           double t_max) {
+                                           double t_max, const float4* s_nodes = nullptr,
+                                           int n_smem = 0) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = __double2float_rd(t_min);
@@ -193,9 +194,21 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     int32_t node = 0;
     for (;;) {
         if (node >= 0) {
-            const float4* p = reinterpret_cast<const float4*>(nodes + node);
-            const float4 a = __ldg(p + 0), b = __ldg(p + 1), c = __ldg(p + 2);
-            const int4 d = __ldg(reinterpret_cast<const int4*>(p + 3));
+            float4 a, b, c;
+            int4 d;
+            if (node < n_smem) {   // top of the tree staged in shared memory
+                const float4* q = s_nodes + 4 * node;
+                a = q[0];
+                b = q[1];
+                c = q[2];
+                d = *reinterpret_cast<const int4*>(q + 3);
+            } else {
+                const float4* p = reinterpret_cast<const float4*>(nodes + node);
+                a = __ldg(p + 0);
+                b = __ldg(p + 1);
+                c = __ldg(p + 2);
+                d = __ldg(reinterpret_cast<const int4*>(p + 3));
+            }
             const float t0 = slab(r, a.x, a.y, a.z, a.w, c.x, c.y, tminf, tb);
             const float t1 = slab(r, b.x, b.y, b.z, b.w, c.z, c.w, tminf, tb);
             const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;

@@ -18,7 +18,8 @@
 
 namespace ef {
 
-constexpr int kTraceThreads = 128;
+constexpr int kTraceThreads = 512;         // one fat CTA per SM (node cache in smem)
+constexpr size_t kNodeCacheBytes = 160 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -68,6 +69,7 @@ struct TraceParams {
     int32_t* path_ids;
     unsigned long long* counter;
     unsigned long long total;
+    int32_t n_smem_nodes;   // BVH nodes [0, n) staged in shared memory
 };
 
 struct LaneStats {
@@ -90,12 +92,19 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned long long* s
 }
 
 template <int NBMAX, int ORDER, bool BRUTE>
-__global__ void __launch_bounds__(kTraceThreads) trace_kernel(const TraceParams P) {
+__global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TraceParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* s_stats = reinterpret_cast<unsigned long long*>(smem);
     double* s_sumt = reinterpret_cast<double*>(s_stats + P.n_src * EF_ST_COUNT);
     double* s_tri = s_sumt + P.n_src;
+    // node cache after the stats, 16-byte aligned
+    float4* s_nodes = reinterpret_cast<float4*>(
+        (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
+    if (!BRUTE) {
+        const float4* g = reinterpret_cast<const float4*>(P.nodes);
+        for (int i = threadIdx.x; i < 4 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
+    }
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0ull;
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
     if (BRUTE)
@@ -158,7 +167,8 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(const TraceParams 
         if (BRUTE)
             h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
         else
-            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
+                                P.n_smem_nodes);
         const bool hit = h.id != INT32_MAX;
         if (P.path_ids) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
@@ -252,7 +262,8 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(const TraceParams 
 // ---------------------------------------------------------------------------
 template <int NBMAX, int ORDER, bool BRUTE>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
-    size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 8 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0);
+    size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 8 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 16 +
+                  (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -537,6 +548,7 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.path_ids = (path_ids && cfg->record_ids) ? path_ids + (size_t)s0 * cfg->n_rays * cfg->max_bounces : nullptr;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
+        P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, kNodeCacheBytes / sizeof(GpuNode));
         if (s->n_bands <= 4)
             e = brute ? dispatch_order<4, true>(cfg->order, P, st) : dispatch_order<4, false>(cfg->order, P, st);
         else
