@@ -60,7 +60,9 @@ enum {
     EF_P_SILENT,           /* 1.0 if the band is silent / indeterminate         */
     EF_P_FIT_N,            /* bins used by the decay regression                 */
     EF_P_SLOPE,            /* dB/s                                              */
-    EF_P_COUNT = 8
+    EF_P_FIRST_BIN,        /* first bin with I_b > 0, -1 if none                */
+    EF_P_LAST_BIN,         /* last bin with I_b > 0, -1 if none                 */
+    EF_P_COUNT = 10
 };
 /* Per-source analysis outputs (f64). */
 enum {
@@ -85,7 +87,7 @@ uint64_t ef_launch_count(void);
  * (n_tri,3) f64 exactly as the reference stores them (scene.py:152-166),
  * material_index (n_tri,) i64, absorption/scattering (n_materials, n_bands)
  * f64 in [0,1] (scene.py:167-170; n_bands generalised from 4 to 1..8).
- * Builds the device BVH (binned SAH, 64-byte two-child nodes, conservative
+ * Builds the device BVH (binned SAH, 128-byte four-child nodes, conservative
  * f32 boxes) and uploads the f64 triangle payload in leaf order. */
 int ef_scene_create(const double* v0, const double* e1, const double* e2,
                     const double* normals, const int64_t* material_index, int64_t n_tri,

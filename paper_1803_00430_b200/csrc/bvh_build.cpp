@@ -5,10 +5,10 @@
 // tree is deliberately NOT the reference's tree: hit ids do not depend on the
 // tree because the leaf test is the reference's exact f64 arithmetic and
 // equal-t ties resolve to the lowest id.  What changes is the
-// layout: two-child nodes holding both child boxes in f32 (64 B, four 16-byte
-// loads per visited node), boxes rounded outward and padded so the f32 slab
+// layout: boxes rounded outward and padded so the f32 slab
 // test never culls a hit the f64 test would accept, SAH over all three axes
-// with 32 bins, and nodes numbered in depth-first order for locality.
+// with 32 bins, then collapsed to 4-wide nodes (128 B, child boxes as f32
+// structure-of-arrays) numbered depth-first for locality.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -51,7 +51,7 @@ struct BNode {
 constexpr int kBins = 32;
 constexpr double kTraverseCost = 1.0;
 constexpr double kIntersectCost = 2.0;   // f64 Moeller-Trumbore vs an f32 box pair
-constexpr int kForceMedianDepth = 40;
+constexpr int kForceMedianDepth = 32;
 
 struct Builder {
     const std::vector<Box>& tb;
@@ -206,63 +206,84 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
     B.nodes.reserve(2 * n);
     int32_t root = B.build(0, n, 0);
 
-    // Convert to two-child device nodes in depth-first order.
+    // Collapse the binary tree into 4-wide device nodes (repeatedly open the
+    // largest inner child until four slots are used), depth-first numbering.
     out.nodes.clear();
     out.order = idx;
-    out.max_depth = B.max_depth;
     out.max_leaf = B.max_leaf;
     auto enc_leaf = [&](const BNode& nd) -> int32_t {
         return ~(int32_t)((nd.start << 3) | (nd.count - 1));
     };
     auto put_box = [&](GpuNode& g, int slot, const Box& b) {
-        float lo[3], hi[3];
-        for (int k = 0; k < 3; ++k) {
-            lo[k] = round_down(b.lo[k] - pad);
-            hi[k] = round_up(b.hi[k] + pad);
+        g.lox[slot] = round_down(b.lo[0] - pad);
+        g.hix[slot] = round_up(b.hi[0] + pad);
+        g.loy[slot] = round_down(b.lo[1] - pad);
+        g.hiy[slot] = round_up(b.hi[1] + pad);
+        g.loz[slot] = round_down(b.lo[2] - pad);
+        g.hiz[slot] = round_up(b.hi[2] + pad);
+    };
+    auto empty_node = []() {
+        GpuNode g;
+        std::memset(&g, 0, sizeof g);
+        for (int c = 0; c < 4; ++c) {
+            g.lox[c] = g.loy[c] = g.loz[c] = 1.0f;   // inverted box, never consulted
+            g.hix[c] = g.hiy[c] = g.hiz[c] = 0.0f;
+            g.child[c] = kEmptyChild;
         }
-        float* xy = slot == 0 ? g.a : g.b;
-        xy[0] = lo[0]; xy[1] = hi[0]; xy[2] = lo[1]; xy[3] = hi[1];
-        g.c[2 * slot + 0] = lo[2];
-        g.c[2 * slot + 1] = hi[2];
+        return g;
     };
     if (B.nodes[root].left < 0) {
-        // single-leaf scene: root with the leaf and an empty (never hit) child
-        GpuNode g;
-        std::memset(&g, 0, sizeof g);
-        // both slots reference the same leaf: an "empty" f32 box is not
-        // reliably rejected by the slab test, a duplicate leaf is harmless
+        GpuNode g = empty_node();
         put_box(g, 0, B.nodes[root].box);
-        put_box(g, 1, B.nodes[root].box);
-        g.d[0] = enc_leaf(B.nodes[root]);
-        g.d[1] = enc_leaf(B.nodes[root]);
+        g.child[0] = enc_leaf(B.nodes[root]);
         out.nodes.push_back(g);
+        out.max_depth = 1;
+        out.max_stack = 1;
         return;
     }
-    // iterative DFS: each inner build node gets the next device slot
-    std::vector<std::pair<int32_t, int32_t>> stack;  // (build node, device slot)
-    out.nodes.push_back(GpuNode());
-    stack.push_back({root, 0});
+    struct Item { int32_t bn; int32_t slot; int depth; };
+    std::vector<Item> stack;
+    out.nodes.push_back(empty_node());
+    stack.push_back({root, 0, 1});
+    int max_depth = 1;
     while (!stack.empty()) {
-        auto [bn, slot] = stack.back();
+        Item it = stack.back();
         stack.pop_back();
-        const BNode& nd = B.nodes[bn];
-        GpuNode g;
-        std::memset(&g, 0, sizeof g);
-        int32_t kids[2] = {nd.left, nd.right};
-        for (int c = 0; c < 2; ++c) {
+        max_depth = std::max(max_depth, it.depth);
+        int32_t kids[4] = {B.nodes[it.bn].left, B.nodes[it.bn].right, -1, -1};
+        int nk = 2;
+        while (nk < 4) {
+            int best = -1;
+            double best_area = -1.0;
+            for (int c = 0; c < nk; ++c) {
+                const BNode& ch = B.nodes[kids[c]];
+                if (ch.left >= 0 && ch.box.half_area() > best_area) {
+                    best_area = ch.box.half_area();
+                    best = c;
+                }
+            }
+            if (best < 0) break;
+            const BNode& op = B.nodes[kids[best]];
+            kids[best] = op.left;
+            kids[nk++] = op.right;
+        }
+        GpuNode g = empty_node();
+        for (int c = 0; c < nk; ++c) {
             const BNode& ch = B.nodes[kids[c]];
             put_box(g, c, ch.box);
             if (ch.left < 0) {
-                g.d[c] = enc_leaf(ch);
+                g.child[c] = enc_leaf(ch);
             } else {
                 int32_t s2 = (int32_t)out.nodes.size();
-                out.nodes.push_back(GpuNode());
-                g.d[c] = s2;
-                stack.push_back({kids[c], s2});
+                out.nodes.push_back(empty_node());
+                g.child[c] = s2;
+                stack.push_back({kids[c], s2, it.depth + 1});
             }
         }
-        out.nodes[slot] = g;
+        out.nodes[it.slot] = g;
     }
+    out.max_depth = max_depth;
+    out.max_stack = 3 * max_depth + 1;   // at most three pushes per level
 }
 
 }  // namespace ef

@@ -1,5 +1,6 @@
-// K4: per-(source, band) decay-fit reducer.  One CTA per source, one warp
-// per band; every reduction is a warp-level segmented sum in f64.
+// K4: per-(source, band) decay-fit reducer.  One 256-thread CTA per
+// (source, band); every reduction is a warp-shuffle + shared-memory sum in f64,
+// the Schroeder integral a block-wide suffix scan over contiguous bin chunks.
 //
 // Replaces (SPEC-only in the reference, pinned in DESIGN.md 3.6):
 //   estimate_rt60           SPEC.md:272-280 (decisions 344-346)
@@ -41,41 +42,62 @@ struct AnalyzeParams {
     double* src_params;
     double* avg_dir;
     double* loudness;
+    int* counters;   // (n_sources) zeroed scratch, reset by the kernel
 };
 
+constexpr int kAThreads = 256;
+constexpr int kAWarps = kAThreads / 32;
+
+// block-wide sum of one double (all threads get the result)
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < kAWarps; ++i) t += red[i];
+    return t;
+}
+
 template <int ORDER>
-__global__ void analyze_kernel(const AnalyzeParams P) {
+__global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
     __shared__ double s_B[kMaxDesign * NK];
-    __shared__ double s_g[kMaxBands][kMaxDesign];
-    __shared__ int s_first;
-    const int s = blockIdx.x;
-    const int b = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
+    __shared__ double s_g[kMaxDesign];
+    __shared__ double s_avg[NK];
+    __shared__ double s_red[kAWarps];
+    __shared__ double s_wsum[kAWarps][NK];
+    __shared__ int s_ired[3][kAWarps];
+    __shared__ double s_dblast;
+    __shared__ int s_done;
     const int nb = P.nb;
+    const int s = blockIdx.x / nb, b = blockIdx.x % nb;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int nbins = P.n_bins;
-    if (threadIdx.x == 0) s_first = INT_MAX;
-    for (int j = threadIdx.x; j < P.n_design; j += blockDim.x) {
+    const float* Hs = P.H + (size_t)s * nbins * nb * NK + (size_t)b * NK;
+    const size_t stride = (size_t)nb * NK;
+    for (int j = tid; j < P.n_design; j += kAThreads) {
         double Y[NK];
         eval_sh<ORDER>(P.design[3 * j], P.design[3 * j + 1], P.design[3 * j + 2], Y);
 #pragma unroll
         for (int k = 0; k < NK; ++k) s_B[j * NK + k] = Y[k];
     }
-    __syncthreads();
+    if (tid == 0) s_dblast = 0.0;
 
-    const float* Hs = P.H + (size_t)s * nbins * nb * NK + b * NK;
-    const size_t stride = (size_t)nb * NK;
-
-    // ---- pass 1: support of I_b(t) = H[t,b,0] / Y00 and directivity sums
+    // ---- pass 1 (contiguous chunk per thread): support of I_b(t) =
+    // H[t,b,0]/Y00 and the directivity sums
+    const int chunk = (nbins + kAThreads - 1) / kAThreads;
+    const int lo = min(tid * chunk, nbins), hi = min(lo + chunk, nbins);
     int last = -1, first = INT_MAX, nnz = 0;
     double S[NK];
 #pragma unroll
     for (int k = 0; k < NK; ++k) S[k] = 0.0;
-    for (int t = lane; t < nbins; t += 32) {
+    for (int t = lo; t < hi; ++t) {
         const float* row = Hs + t * stride;
-        const double I = (double)row[0] / kY00;
-        if (I > 0.0) {
-            last = max(last, t);
+        if ((double)row[0] / kY00 > 0.0) {
+            last = t;
             first = min(first, t);
             ++nnz;
         }
@@ -90,32 +112,59 @@ __global__ void analyze_kernel(const AnalyzeParams P) {
     }
 #pragma unroll
     for (int k = 0; k < NK; ++k) S[k] = warp_sum(S[k]);
-    const double total = S[0] / kY00;
+    if (lane == 0) {
+        s_ired[0][w] = last;
+        s_ired[1][w] = first;
+        s_ired[2][w] = nnz;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) s_wsum[w][k] = S[k];
+    }
+    __syncthreads();
+    last = -1; first = INT_MAX; nnz = 0;
+#pragma unroll
+    for (int i = 0; i < kAWarps; ++i) {
+        last = max(last, s_ired[0][i]);
+        first = min(first, s_ired[1][i]);
+        nnz += s_ired[2][i];
+    }
+    if (tid < NK) {
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < kAWarps; ++i) a += s_wsum[i][tid];
+        s_avg[tid] = a;   // raw sums for now
+    }
+    __syncthreads();
+    const double total = s_avg[0] / kY00;
 
     // ---- pass 2: Schroeder backward integration from the last non-zero bin
-    // (truncation) and least-squares fits on [-35,-5] / [-25,-5] dB
+    // (truncation); LS fits on [-35,-5] and [-25,-5] dB
     double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
     double db_last = 0.0;
-    if (nnz >= 3) {
-        const int len = last + 1;
-        const int chunk = (len + 31) / 32;
-        const int lo = min(lane * chunk, len), hi = min(lo + chunk, len);
+    const bool enough = nnz >= 3;
+    if (enough) {
+        const int h2 = min(hi, last + 1);
         double csum = 0.0;
-        for (int t = hi - 1; t >= lo; --t) csum += (double)Hs[t * stride] / kY00;
-        // inclusive suffix scan over lanes (lane l: sum of chunks l..31)
+        for (int t = h2 - 1; t >= lo; --t) csum += (double)Hs[t * stride] / kY00;
+        // block inclusive suffix scan of the chunk sums
         double suf = csum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const double v = __shfl_down_sync(kAll, suf, o);
             if (lane + o < 32) suf += v;
         }
-        const double edc0 = __shfl_sync(kAll, suf, 0);
-        double acc = suf - csum;   // energy after this lane's chunk
-        for (int t = hi - 1; t >= lo; --t) {
+        if (lane == 0) s_red[w] = suf;   // warp total
+        __syncthreads();
+        double after = 0.0;
+        for (int i = w + 1; i < kAWarps; ++i) after += s_red[i];
+        suf += after;
+        double edc0 = 0.0;
+        for (int i = 0; i < kAWarps; ++i) edc0 += s_red[i];
+        double acc = suf - csum;   // energy after this thread's chunk
+        for (int t = h2 - 1; t >= lo; --t) {
             acc += (double)Hs[t * stride] / kY00;
             const double db = 10.0 * log10(acc / edc0);
             const double x = (double)t * P.bin_s;
-            if (t == last) db_last = db;
+            if (t == last) s_dblast = db;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const double lim = r == 0 ? -35.0 : -25.0;
@@ -131,12 +180,12 @@ __global__ void analyze_kernel(const AnalyzeParams P) {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int i = 0; i < 5; ++i) fit[r][i] = warp_sum(fit[r][i]);
-        db_last = warp_sum(db_last);   // only the owner of `last` contributes
+            for (int i = 0; i < 5; ++i) fit[r][i] = block_sum(fit[r][i], s_red);
+        db_last = s_dblast;
     }
 
-    // ---- per-band outputs (lane 0 writes)
-    bool silent = nnz < 3;
+    // ---- per-band outputs
+    bool silent = !enough;
     double slope = 0.0, nfit = 0.0;
     if (!silent) {
         const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
@@ -162,8 +211,8 @@ __global__ void analyze_kernel(const AnalyzeParams P) {
     if (!(edir > 0.0)) drr = -99.0;
     else if (!(total > 0.0)) drr = 99.0;
     else drr = fmin(fmax(10.0 * log10(edir / total), -99.0), 99.0);
-    if (lane == 0) {
-        double* p = P.params + ((size_t)s * nb + b) * EF_P_COUNT;
+    double* p = P.params + ((size_t)s * nb + b) * EF_P_COUNT;
+    if (tid == 0) {
         p[EF_P_RT60] = rt60;
         p[EF_P_GAIN] = gain;
         p[EF_P_DRR_DB] = drr;
@@ -172,44 +221,52 @@ __global__ void analyze_kernel(const AnalyzeParams P) {
         p[EF_P_SILENT] = silent ? 1.0 : 0.0;
         p[EF_P_FIT_N] = nfit;
         p[EF_P_SLOPE] = slope;
-        if (first != INT_MAX) atomicMin(&s_first, first);
+        p[EF_P_FIRST_BIN] = first == INT_MAX ? -1.0 : (double)first;
+        p[EF_P_LAST_BIN] = (double)last;
     }
 
     // ---- average directivity and loudness (sh.py:240-253)
-    double avg[NK];
-#pragma unroll
-    for (int k = 0; k < NK; ++k) avg[k] = total > 0.0 ? S[k] / total : 0.0;
-    if (lane == 0 && P.avg_dir) {
-        double* a = P.avg_dir + ((size_t)s * nb + b) * NK;
-#pragma unroll
-        for (int k = 0; k < NK; ++k) a[k] = avg[k];
-    }
+    __syncthreads();
+    if (tid < NK) s_avg[tid] = total > 0.0 ? s_avg[tid] / total : 0.0;
+    __syncthreads();
+    if (tid < NK && P.avg_dir) P.avg_dir[((size_t)s * nb + b) * NK + tid] = s_avg[tid];
     if (P.loudness) {
-        for (int j = lane; j < P.n_design; j += 32) {
+        for (int j = tid; j < P.n_design; j += kAThreads) {
             double g = 0.0;
 #pragma unroll
-            for (int k = 0; k < NK; ++k) g += s_B[j * NK + k] * avg[k];
-            s_g[b][j] = fmax(0.0, g);
+            for (int k = 0; k < NK; ++k) g += s_B[j * NK + k] * s_avg[k];
+            s_g[j] = fmax(0.0, g);
         }
-        __syncwarp();
+        __syncthreads();
         const double scale = 4.0 * M_PI / (double)P.n_design;
         double* D = P.loudness + ((size_t)s * nb + b) * NK * NK;
-        for (int e = lane; e < NK * NK; e += 32) {
+        for (int e = tid; e < NK * NK; e += kAThreads) {
             const int k1 = e / NK, k2 = e % NK;
             double acc = 0.0;
-            for (int j = 0; j < P.n_design; ++j) acc += s_B[j * NK + k1] * s_g[b][j] * s_B[j * NK + k2];
+            for (int j = 0; j < P.n_design; ++j) acc += s_B[j * NK + k1] * s_g[j] * s_B[j * NK + k2];
             D[e] = scale * acc;
         }
     }
-    // ---- per-source outputs
+
+    // ---- per-source outputs: the last band block of a source finishes it
+    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) s_done = atomicAdd(P.counters + s, 1);
+    __syncthreads();
+    if (s_done == nb - 1 && tid == 0) {
+        __threadfence();
+        double firstb = -1.0;
+        for (int bb = 0; bb < nb; ++bb) {
+            const double f = ((volatile double*)P.params)[((size_t)s * nb + bb) * EF_P_COUNT + EF_P_FIRST_BIN];
+            if (f >= 0.0 && (firstb < 0.0 || f < firstb)) firstb = f;
+        }
         double* q = P.src_params + (size_t)s * EF_S_COUNT;
-        q[EF_S_PREDELAY] = s_first == INT_MAX ? -1.0 : (double)s_first * P.bin_s;
+        q[EF_S_PREDELAY] = firstb < 0.0 ? -1.0 : firstb * P.bin_s;
         const unsigned long long nrefl = P.stats[(size_t)s * EF_ST_COUNT + EF_ST_REFLECTIONS];
         q[EF_S_MFP] = nrefl ? P.sum_t[s] / (double)nrefl : 0.0;
-        q[EF_S_SILENT] = s_first == INT_MAX ? 1.0 : 0.0;
+        q[EF_S_SILENT] = firstb < 0.0 ? 1.0 : 0.0;
         q[3] = 0.0;
+        P.counters[s] = 0;
     }
 }
 
@@ -248,10 +305,14 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
     if (loudness && (!design || n_design < 1 || n_design > kMaxDesign))
         return set_error(EF_EINVAL, "ef_analyze: loudness needs a t-design of 1..64 directions");
     if (!(cfg->bin_s > 0.0) || !(cfg->max_rt >= 0.05)) return set_error(EF_EINVAL, "ef_analyze: bad bin_s / max_rt");
-    AnalyzeParams P{H, Dir, stats, sum_t, design, loudness ? n_design : 0, cfg->n_bins, cfg->n_bands,
-                    cfg->bin_s, cfg->max_rt, params, src_params, avg_dir, loudness};
     cudaStream_t st = (cudaStream_t)stream;
-    const dim3 grid(cfg->n_sources), block(32 * cfg->n_bands);
+    int* counters = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&counters, sizeof(int) * cfg->n_sources, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, sizeof(int) * cfg->n_sources, st);
+    if (e != cudaSuccess) return check_cuda(e, "ef_analyze scratch");
+    AnalyzeParams P{H, Dir, stats, sum_t, design, loudness ? n_design : 0, cfg->n_bins, cfg->n_bands,
+                    cfg->bin_s, cfg->max_rt, params, src_params, avg_dir, loudness, counters};
+    const dim3 grid(cfg->n_sources * cfg->n_bands), block(kAThreads);
     switch (cfg->order) {
         case 0: analyze_kernel<0><<<grid, block, 0, st>>>(P); break;
         case 1: analyze_kernel<1><<<grid, block, 0, st>>>(P); break;
@@ -259,6 +320,8 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
         case 3: analyze_kernel<3><<<grid, block, 0, st>>>(P); break;
         default: analyze_kernel<4><<<grid, block, 0, st>>>(P); break;
     }
+    cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(counters, st);
     count_launch();
-    return check_cuda(cudaGetLastError(), "analyze_kernel");
+    return check_cuda(le, "analyze_kernel");
 }

@@ -160,9 +160,50 @@ __device__ __forceinline__ RayF make_rayf(double ox, double oy, double oz, doubl
     return r;
 }
 
-// Conservative slab test of one f32 box; returns entry distance or +inf.
-__device__ __forceinline__ float slab(const RayF& r, float lox, float hix, float loy, float hiy,
-                                      float loz, float hiz, float tmin, float tmax) {
+struct Hit {
+    double t;
+    int32_t id;  // original triangle id, INT32_MAX = none
+};
+
+// The reference's Moeller-Trumbore decision (bvh.py:17-27) restricted to
+// t in (t_min, t_hi], with a division-free conservative pre-rejection: the
+// unnormalised U, V, T are compared against |det|-scaled bounds with a 2x
+// margin, so a candidate is only dropped early when the exact test would
+// drop it too; survivors take the bit-exact path (1/det, u, v, t).
+__device__ __forceinline__ bool mt_hit(double ox, double oy, double oz, double dx, double dy,
+                                       double dz, const double* __restrict__ v, double t_min,
+                                       double t_hi, double& t) {
+    const double v0x = v[0], v0y = v[1], v0z = v[2];
+    const double e1x = v[3], e1y = v[4], e1z = v[5];
+    const double e2x = v[6], e2y = v[7], e2z = v[8];
+    const double px = dy * e2z - dz * e2y;
+    const double py = dz * e2x - dx * e2z;
+    const double pz = dx * e2y - dy * e2x;
+    const double det = dot3(e1x, e1y, e1z, px, py, pz);
+    const double tx = ox - v0x, ty = oy - v0y, tz = oz - v0z;
+    const double U = dot3(tx, ty, tz, px, py, pz);
+    const double qx = ty * e1z - tz * e1y;
+    const double qy = tz * e1x - tx * e1z;
+    const double qz = tx * e1y - ty * e1x;
+    const double V = dot3(qx, qy, qz, dx, dy, dz);
+    const double T = dot3(e2x, e2y, e2z, qx, qy, qz);
+    const double ad = fabs(det);
+    if (!(ad > 1e-14)) return false;
+    const double sg = det > 0.0 ? 1.0 : -1.0;
+    const double Ua = U * sg, Va = V * sg, Ta = T * sg;
+    if (Ua < -2e-10 * ad || Va < -2e-10 * ad || Ua + Va > (1.0 + 2e-10) * ad ||
+        Ta <= 0.5 * t_min * ad || Ta > t_hi * ad * (1.0 + 1e-9))
+        return false;
+    const double inv = 1.0 / det;
+    const double u = U * inv;
+    const double vv = V * inv;
+    if (!(u >= -1e-10) || !(vv >= -1e-10) || !(u + vv <= 1.0 + 1e-10)) return false;
+    t = T * inv;
+    return t > t_min && t <= t_hi;
+}
+
+__device__ __forceinline__ float slab1(const RayF& r, float lox, float hix, float loy, float hiy,
+                                       float loz, float hiz, float tmin, float tmax) {
     const float x0 = __fmaf_rn(lox, r.ix, -r.ox), x1 = __fmaf_rn(hix, r.ix, -r.ox);
     const float y0 = __fmaf_rn(loy, r.iy, -r.oy), y1 = __fmaf_rn(hiy, r.iy, -r.oy);
     const float z0 = __fmaf_rn(loz, r.iz, -r.oz), z1 = __fmaf_rn(hiz, r.iz, -r.oz);
@@ -171,14 +212,43 @@ __device__ __forceinline__ float slab(const RayF& r, float lox, float hix, float
     return tn <= __fmul_rn(tf, 1.0000038f) ? tn : INFINITY;
 }
 
-struct Hit {
-    double t;
-    int32_t id;  // original triangle id, INT32_MAX = none
-};
+__device__ __forceinline__ void cswap(float& ta, int32_t& ca, float& tb, int32_t& cb) {
+    const bool s = tb < ta;
+    const float t = ta;
+    const int32_t c = ca;
+    ta = s ? tb : ta;
+    ca = s ? cb : ca;
+    tb = s ? t : tb;
+    cb = s ? c : cb;
+}
 
-// Closest hit over the device BVH.  Accepts t in (t_min, t_max]; equal t
-// resolves to the lowest triangle id, so the answer is independent of the
-// tree and of the traversal order.
+// Leaf: exact tests of up to 8 consecutive triangles of the leaf-ordered
+// payload; equal t resolves to the lowest original id.
+__device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32_t enc, double ox,
+                                          double oy, double oz, double dx, double dy, double dz,
+                                          double t_min, Hit& h, float& tb) {
+    const uint32_t e = ~(uint32_t)enc;
+    const uint32_t start = e >> 3, cnt = (e & 7u) + 1u;
+    for (uint32_t i = 0; i < cnt; ++i) {
+        const double2* q = reinterpret_cast<const double2*>(tris + start + i);
+        const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3),
+                      q4 = __ldg(q + 4);
+        const double v[9] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y, q4.x};
+        const int32_t id = (int32_t)__double_as_longlong(q4.y);
+        double t;
+        if (mt_hit(ox, oy, oz, dx, dy, dz, v, t_min, h.t, t) && (t < h.t || id < h.id)) {
+            h.t = t;
+            h.id = id;
+            tb = __double2float_ru(t);
+        }
+    }
+}
+
+// Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
+// equal t resolves to the lowest triangle id, so the answer is independent of
+// the tree and of the traversal order.  Children are visited
+// nearest-first (4-input sorting network); nodes [0, n_smem) are read from
+// the shared-memory copy of the top of the tree.
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
@@ -194,56 +264,37 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     int32_t node = 0;
     for (;;) {
         if (node >= 0) {
-            float4 a, b, c;
-            int4 d;
-            if (node < n_smem) {   // top of the tree staged in shared memory
-                const float4* q = s_nodes + 4 * node;
-                a = q[0];
-                b = q[1];
-                c = q[2];
-                d = *reinterpret_cast<const int4*>(q + 3);
+            float4 lx, hx, ly, hy, lz, hz;
+            int4 ch;
+            if (node < n_smem) {
+                const float4* q = s_nodes + 8 * node;
+                lx = q[0]; hx = q[1]; ly = q[2]; hy = q[3]; lz = q[4]; hz = q[5];
+                ch = *reinterpret_cast<const int4*>(q + 6);
             } else {
-                const float4* p = reinterpret_cast<const float4*>(nodes + node);
-                a = __ldg(p + 0);
-                b = __ldg(p + 1);
-                c = __ldg(p + 2);
-                d = __ldg(reinterpret_cast<const int4*>(p + 3));
+                const float4* q = reinterpret_cast<const float4*>(nodes + node);
+                lx = __ldg(q + 0); hx = __ldg(q + 1); ly = __ldg(q + 2);
+                hy = __ldg(q + 3); lz = __ldg(q + 4); hz = __ldg(q + 5);
+                ch = __ldg(reinterpret_cast<const int4*>(q + 6));
             }
-            const float t0 = slab(r, a.x, a.y, a.z, a.w, c.x, c.y, tminf, tb);
-            const float t1 = slab(r, b.x, b.y, b.z, b.w, c.z, c.w, tminf, tb);
-            const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
-            if (h0 && h1) {
-                const bool first0 = t0 <= t1;
-                stack_node[sp] = first0 ? d.y : d.x;
-                stack_t[sp] = first0 ? t1 : t0;
-                ++sp;
-                node = first0 ? d.x : d.y;
-                continue;
-            }
-            if (h0 || h1) {
-                node = h0 ? d.x : d.y;
+            float t0 = ch.x != kEmptyChild ? slab1(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tminf, tb) : INFINITY;
+            float t1 = ch.y != kEmptyChild ? slab1(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tminf, tb) : INFINITY;
+            float t2 = ch.z != kEmptyChild ? slab1(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tminf, tb) : INFINITY;
+            float t3 = ch.w != kEmptyChild ? slab1(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tminf, tb) : INFINITY;
+            int32_t c0 = ch.x, c1 = ch.y, c2 = ch.z, c3 = ch.w;
+            cswap(t0, c0, t1, c1);
+            cswap(t2, c2, t3, c3);
+            cswap(t0, c0, t2, c2);
+            cswap(t1, c1, t3, c3);
+            cswap(t1, c1, t2, c2);
+            if (t3 != INFINITY) { stack_node[sp] = c3; stack_t[sp] = t3; ++sp; }
+            if (t2 != INFINITY) { stack_node[sp] = c2; stack_t[sp] = t2; ++sp; }
+            if (t1 != INFINITY) { stack_node[sp] = c1; stack_t[sp] = t1; ++sp; }
+            if (t0 != INFINITY) {
+                node = c0;
                 continue;
             }
         } else {
-            const uint32_t enc = ~(uint32_t)node;
-            const uint32_t start = enc >> 3, cnt = (enc & 7u) + 1u;
-            for (uint32_t i = 0; i < cnt; ++i) {
-                const GpuTri* tp = tris + start + i;
-                double v[9];
-                const double2* q = reinterpret_cast<const double2*>(tp);
-                const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2),
-                              q3 = __ldg(q + 3), q4 = __ldg(q + 4);
-                v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y; v[4] = q2.x;
-                v[5] = q2.y; v[6] = q3.x; v[7] = q3.y; v[8] = q4.x;
-                const int32_t id = (int32_t)__double_as_longlong(q4.y);
-                double t;
-                if (mt_exact(ox, oy, oz, dx, dy, dz, v, t) && t > t_min && t <= h.t &&
-                    (t < h.t || id < h.id)) {
-                    h.t = t;
-                    h.id = id;
-                    tb = __double2float_ru(t);
-                }
-            }
+            leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb);
         }
         // pop the next node still in front of the current closest hit
         for (;;) {

@@ -1,5 +1,6 @@
 // Internal structures shared by the host builder and the CUDA kernels.
 #pragma once
+#include <climits>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -12,22 +13,23 @@ constexpr int kMaxBands = 8;
 constexpr int kMaxOrder = 4;
 constexpr int kBruteMaxTris = 512;   // scene.py:29
 constexpr double kRayEps = 1e-4;     // scene.py:22
-constexpr int kStackSize = 64;
+constexpr int kStackSize = 96;
 constexpr int kMaxLeaf = 4;
 
-// Two-child BVH node, 64 bytes (four 16-byte vectors):
-//   a = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
-//   b = (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
-//   c = (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)
-//   d = (child0, child1, -, -)  child >= 0: inner node index,
-//                               child <  0: leaf ~((start << 3) | (count - 1))
+// Four-child BVH node, 128 bytes = eight 16-byte vectors, child boxes in
+// structure-of-arrays form so one node visit is 7 vector loads and four
+// independent slab tests:
+//   lox, hix, loy, hiy, loz, hiz : float[4]  (conservative f32 child boxes)
+//   child : int32[4]  >= 0 inner node index,
+//                     <  0 leaf ~((start << 3) | (count - 1)),
+//                     kEmptyChild = unused slot
 struct alignas(16) GpuNode {
-    float a[4];
-    float b[4];
-    float c[4];
-    int32_t d[4];
+    float lox[4], hix[4], loy[4], hiy[4], loz[4], hiz[4];
+    int32_t child[4];
+    int32_t pad[4];
 };
-static_assert(sizeof(GpuNode) == 64, "node must be 64 bytes");
+static_assert(sizeof(GpuNode) == 128, "node must be 128 bytes");
+constexpr int32_t kEmptyChild = INT32_MIN;
 
 // f64 triangle payload in BVH leaf order, 80 bytes = 5 x double2:
 // v0.xyz e1.xyz e2.xyz and the original triangle id (as int64 bits).
@@ -40,8 +42,9 @@ static_assert(sizeof(GpuTri) == 80, "tri must be 80 bytes");
 struct HostBvh {
     std::vector<GpuNode> nodes;
     std::vector<int64_t> order;  // leaf-order position -> original triangle id
-    int max_depth = 0;
+    int max_depth = 0;           // of the 4-wide tree
     int max_leaf = 0;
+    int max_stack = 0;           // bound on traversal stack entries
 };
 
 // Builds a binned-SAH BVH2 with conservative f32 boxes over the triangles

@@ -32,8 +32,7 @@ __device__ __forceinline__ Hit closest_brute(const double* __restrict__ s_tri, i
     Hit h{INFINITY, INT32_MAX};
     for (int i = 0; i < n; ++i) {
         double t;
-        if (mt_exact(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t) && t > t_min && t <= t_max &&
-            t < h.t) {
+        if (mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, fmin(t_max, h.t), t) && t < h.t) {
             h.t = t;
             h.id = i;
         }
@@ -103,7 +102,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
     if (!BRUTE) {
         const float4* g = reinterpret_cast<const float4*>(P.nodes);
-        for (int i = threadIdx.x; i < 4 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
+        for (int i = threadIdx.x; i < 8 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
     }
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0ull;
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
