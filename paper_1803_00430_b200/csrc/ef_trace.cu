@@ -77,12 +77,12 @@ struct LaneStats {
     double sum_t = 0.0;
 };
 
-__device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned long long* s_stats,
+__device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats,
                                             double* s_sumt) {
     if (ls.src >= 0) {
 #pragma unroll
         for (int i = 0; i < EF_ST_COUNT; ++i)
-            if (ls.c[i]) atomicAdd(&s_stats[ls.src * EF_ST_COUNT + i], (unsigned long long)ls.c[i]);
+            if (ls.c[i]) atomicAdd(&s_stats[ls.src * EF_ST_COUNT + i], ls.c[i]);   // native 32-bit ATOMS
         if (ls.sum_t != 0.0) atomicAdd(&s_sumt[ls.src], ls.sum_t);
     }
 #pragma unroll
@@ -94,9 +94,12 @@ template <int NBMAX, int ORDER, bool BRUTE>
 __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TraceParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* s_stats = reinterpret_cast<unsigned long long*>(smem);
-    double* s_sumt = reinterpret_cast<double*>(s_stats + P.n_src * EF_ST_COUNT);
-    double* s_tri = s_sumt + P.n_src;
+    // per-block counters: f64 path-length sums, then u32 counters (a block's
+    // per-source counts stay far below 2^32), then the all-pairs triangles
+    double* s_sumt = reinterpret_cast<double*>(smem);
+    unsigned int* s_stats = reinterpret_cast<unsigned int*>(s_sumt + P.n_src);
+    double* s_tri = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(s_stats + P.n_src * EF_ST_COUNT) + 15) & ~uintptr_t(15));
     // node cache after the stats, 16-byte aligned
     float4* s_nodes = reinterpret_cast<float4*>(
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
         const float4* g = reinterpret_cast<const float4*>(P.nodes);
         for (int i = threadIdx.x; i < 8 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
     }
-    for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0ull;
+    for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0u;
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
     if (BRUTE)
         for (int i = threadIdx.x; i < 9 * P.n_tri; i += blockDim.x) s_tri[i] = P.tris_by_id[i];
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
     flush_stats(ls, s_stats, s_sumt);
     __syncthreads();
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x)
-        if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
+        if (s_stats[i]) atomicAdd(P.stats + i, (unsigned long long)s_stats[i]);
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x)
         if (s_sumt[i] != 0.0) atomicAdd(P.sum_t + i, s_sumt[i]);
 }
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
 // ---------------------------------------------------------------------------
 template <int NBMAX, int ORDER, bool BRUTE>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
-    size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 8 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 16 +
+    size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
                   (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
     if (smem > 48 * 1024) {

@@ -1,0 +1,56 @@
+"""Probe where the C2 frame time goes: vary the bounce cap (tail) and the
+ray count (bulk) and time ef_trace alone with CUDA events.
+
+    python tools/probe_trace.py [config]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1803_00430_b200 import propagation, workloads  # noqa: E402
+from paper_1803_00430_b200.scene import scene_from_workload  # noqa: E402
+
+
+def time_trace(tr, w, reps=20, **kw):
+    for _ in range(3):
+        tr.trace(w.listener, **kw)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        a.record()
+        tr.trace(w.listener, **kw)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    segs = int(tr.stats[:, 1].sum())
+    return float(np.median(ts)), segs
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    w = workloads.WORKLOADS[name]()
+    sc = scene_from_workload(w)
+    print("scene", sc.device_info())
+    for mb in (1, 2, 5, 10, 20, 50, 100):
+        cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=mb, sh_order=w.order,
+                                      bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius,
+                                      seed=w.seed)
+        tr = propagation.FrameTracer(sc, len(w.sources), cfg)
+        tr.set_sources(w.sources)
+        ms, segs = time_trace(tr, w)
+        print(f"max_bounces {mb:4d}: {ms*1e3:8.1f} us  segs {segs:9d}  {segs/ms/1e6:7.3f} Gseg/s")
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    for mult in (1, 2, 4, 8, 16):
+        tr = propagation.FrameTracer(sc, len(w.sources), cfg)
+        tr.set_sources(w.sources)
+        ms, segs = time_trace(tr, w, n_rays=w.n_rays * mult)
+        print(f"rays x{mult:3d}: {ms*1e3:8.1f} us  segs {segs:9d}  {segs/ms/1e6:7.3f} Gseg/s")
+
+
+if __name__ == "__main__":
+    main()
