@@ -20,6 +20,7 @@ namespace ef {
 
 constexpr int kTraceThreads = 512;         // one fat CTA per SM (node cache in smem)
 constexpr size_t kNodeCacheBytes = 160 * 1024;
+constexpr size_t kMaxTraceSmem = 200 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -69,7 +70,14 @@ struct TraceParams {
     unsigned long long* counter;
     unsigned long long total;
     int32_t n_smem_nodes;   // BVH nodes [0, n) staged in shared memory
+    int32_t timing;         // debug: path_ids rows get (t0, t1, smid, nseg)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct LaneStats {
     int src = -1;
@@ -124,6 +132,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
     uint32_t ray = 0, skey = 0;
     int src = 0, nrefl = 0, nseg = 0;
     unsigned long long path = 0;
+    unsigned long long t_start = 0;
 
     for (;;) {
         // ---- warp-aggregated refill: idle lanes take the next path indices
@@ -157,6 +166,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
                         ls.src = src;
                     }
                     ls.c[EF_ST_PATHS]++;
+                    if (P.timing) t_start = globaltimer();
                     active = true;
                 }
             }
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
             h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
                                 P.n_smem_nodes);
         const bool hit = h.id != INT32_MAX;
-        if (P.path_ids) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
+        if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
         // ---- listener sphere receiver + SH histogram commit
         {
@@ -252,6 +262,18 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
             if (nrefl >= P.max_bounces) active = false;
         }
         if (!active && P.path_nseg) P.path_nseg[path] = nseg;
+        if (!active && P.timing) {
+            const unsigned long long t_end = globaltimer();
+            int32_t* row = P.path_ids + path * P.max_bounces;
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            row[0] = (int32_t)(t_start & 0xffffffffu);
+            row[1] = (int32_t)(t_start >> 32);
+            row[2] = (int32_t)(t_end & 0xffffffffu);
+            row[3] = (int32_t)(t_end >> 32);
+            row[4] = (int32_t)smid;
+            row[5] = nseg;
+        }
     }
     flush_stats(ls, s_stats, s_sumt);
     __syncthreads();
@@ -262,23 +284,32 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
 }
 
 // ---------------------------------------------------------------------------
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
 template <int NBMAX, int ORDER, bool BRUTE>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
                   (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr_done = false;   // once per instantiation: no per-launch host queries
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kMaxTraceSmem);
         if (e != cudaSuccess) return e;
+        attr_done = true;
     }
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTraceThreads, smem);
-    if (e != cudaSuccess) return e;
-    per_sm = std::max(per_sm, 1);
-    // persistent grid: every SM fully occupied, no more warps than paths
-    long long want = (long long)sms * per_sm;
+    if (smem > kMaxTraceSmem) return cudaErrorInvalidValue;
+    // persistent grid: one 512-thread CTA per SM (__launch_bounds__(512, 1)
+    // and ~100 registers leave room for exactly one), no more warps than paths
+    long long want = (long long)sm_count();
     long long need = ((long long)P.total + kTraceThreads - 1) / kTraceThreads;
     int grid = (int)std::max(1LL, std::min(want, need));
     kern<<<grid, kTraceThreads, smem, st>>>(P);
@@ -548,6 +579,7 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
         P.path_ids = (path_ids && cfg->record_ids) ? path_ids + (size_t)s0 * cfg->n_rays * cfg->max_bounces : nullptr;
+        P.timing = (P.path_ids && cfg->record_ids == 2 && cfg->max_bounces >= 6) ? 1 : 0;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
         P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, kNodeCacheBytes / sizeof(GpuNode));

@@ -52,5 +52,42 @@ def main():
         print(f"rays x{mult:3d}: {ms*1e3:8.1f} us  segs {segs:9d}  {segs/ms/1e6:7.3f} Gseg/s")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) <= 2:
     main()
+
+
+def timing(name="c2"):
+    """Per-path start/end (globaltimer ns) of one full frame."""
+    w = workloads.WORKLOADS[name]()
+    sc = scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = propagation.FrameTracer(sc, len(w.sources), cfg, record=2)
+    tr.set_sources(w.sources)
+    for _ in range(3):
+        tr.trace(w.listener)
+    torch.cuda.synchronize()
+    rows = tr.path_ids.cpu().numpy().reshape(-1, w.max_bounces)[:, :6].astype(np.int64)
+    t0 = (rows[:, 0] & 0xffffffff) | (rows[:, 1] << 32)
+    t1 = (rows[:, 2] & 0xffffffff) | (rows[:, 3] << 32)
+    base = t0.min()
+    t0 = (t0 - base) / 1e3
+    t1 = (t1 - base) / 1e3
+    nseg = rows[:, 5]
+    dur = t1 - t0
+    print(f"[{name}] span {t1.max():.1f} us; last path start {t0.max():.1f} us; "
+          f"paths done by: 50% {np.percentile(t1, 50):.1f} 90% {np.percentile(t1, 90):.1f} "
+          f"99% {np.percentile(t1, 99):.1f} 99.9% {np.percentile(t1, 99.9):.1f} 100% {t1.max():.1f}")
+    order = np.argsort(-t1)[:8]
+    for i in order:
+        print(f"  path {i}: start {t0[i]:.1f} end {t1[i]:.1f} dur {dur[i]:.1f} us nseg {nseg[i]} "
+              f"({dur[i] / max(nseg[i], 1):.2f} us/seg) sm {rows[i, 4]}")
+    for k in (1, 2, 4, 10, 50):
+        sel = nseg == k
+        if sel.any():
+            print(f"  nseg={k:3d}: n={sel.sum():6d} mean dur {dur[sel].mean():.2f} us "
+                  f"({dur[sel].mean() / k:.2f} us/seg)")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "timing":
+    timing(sys.argv[1])
