@@ -91,3 +91,25 @@ def timing(name="c2"):
 
 if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "timing":
     timing(sys.argv[1])
+
+
+def single(name="c2", src=6, ray=27707, reps=5):
+    """One path alone on the GPU: in-kernel duration and per-segment latency."""
+    w = workloads.WORKLOADS[name]()
+    sc = scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = propagation.FrameTracer(sc, 1, cfg, record=2)
+    tr.set_sources(w.sources[src:src + 1], [src])
+    for _ in range(reps):
+        tr.trace(w.listener, ray_ids=[ray])
+        torch.cuda.synchronize()
+        r = tr.path_ids.cpu().numpy().reshape(-1)[:6].astype(np.int64)
+        t0 = (r[0] & 0xffffffff) | (r[1] << 32)
+        t1 = (r[2] & 0xffffffff) | (r[3] << 32)
+        print(f"[{name}] single path src {src} ray {ray}: {(t1 - t0) / 1e3:.1f} us, nseg {r[5]}, "
+              f"{(t1 - t0) / 1e3 / r[5]:.2f} us/seg")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "single":
+    single(sys.argv[1])
