@@ -226,8 +226,9 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
         GpuNode g;
         std::memset(&g, 0, sizeof g);
         for (int c = 0; c < 4; ++c) {
-            g.lox[c] = g.loy[c] = g.loz[c] = 1.0f;   // inverted box, never consulted
-            g.hix[c] = g.hiy[c] = g.hiz[c] = 0.0f;
+            // lo = +inf, hi = -inf: both sign-selected planes give t_near = +inf
+            g.lox[c] = g.loy[c] = g.loz[c] = INFINITY;
+            g.hix[c] = g.hiy[c] = g.hiz[c] = -INFINITY;
             g.child[c] = kEmptyChild;
         }
         return g;

@@ -140,6 +140,7 @@ __device__ __forceinline__ bool mt_full(double ox, double oy, double oz, double 
 struct RayF {
     float ox, oy, oz;    // origin * inv (for the FMA slab form)
     float ix, iy, iz;    // 1 / direction
+    int nx, ny, nz;      // float4 index of the near plane per axis (far = near ^ 1)
 };
 
 __device__ __forceinline__ float safe_inv(double d) {
@@ -157,7 +158,23 @@ __device__ __forceinline__ RayF make_rayf(double ox, double oy, double oz, doubl
     r.ox = __fmul_rn((float)ox, r.ix);
     r.oy = __fmul_rn((float)oy, r.iy);
     r.oz = __fmul_rn((float)oz, r.iz);
+    // node layout lox,hix,loy,hiy,loz,hiz: the near plane of an axis is its
+    // lo plane for a positive direction, its hi plane otherwise
+    r.nx = r.ix >= 0.0f ? 0 : 1;
+    r.ny = r.iy >= 0.0f ? 2 : 3;
+    r.nz = r.iz >= 0.0f ? 4 : 5;
     return r;
+}
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));   // FMNMX3 (sm_100)
+    return d;
+}
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
 
 struct Hit {
@@ -202,24 +219,28 @@ __device__ __forceinline__ bool mt_hit(double ox, double oy, double oz, double d
     return t > t_min && t <= t_hi;
 }
 
-__device__ __forceinline__ float slab1(const RayF& r, float lox, float hix, float loy, float hiy,
-                                       float loz, float hiz, float tmin, float tmax) {
-    const float x0 = __fmaf_rn(lox, r.ix, -r.ox), x1 = __fmaf_rn(hix, r.ix, -r.ox);
-    const float y0 = __fmaf_rn(loy, r.iy, -r.oy), y1 = __fmaf_rn(hiy, r.iy, -r.oy);
-    const float z0 = __fmaf_rn(loz, r.iz, -r.oz), z1 = __fmaf_rn(hiz, r.iz, -r.oz);
-    const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));
-    const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));
-    return tn <= __fmul_rn(tf, 1.0000038f) ? tn : INFINITY;
+// Conservative slab test of one child box from its sign-selected near/far
+// planes; returns a sortable key (t_near bits with the low two bits replaced
+// by the child slot; t_near >= 0 so unsigned order == float order) or
+// 0xffffffff on a miss.  Empty slots hold lo = +inf, hi = -inf and miss.
+__device__ __forceinline__ uint32_t slab_key(const RayF& r, float nx, float fx, float ny, float fy,
+                                             float nz, float fz, float tmin, float tmax,
+                                             uint32_t slot) {
+    const float tn = fmax3f(__fmaf_rn(nx, r.ix, -r.ox), __fmaf_rn(ny, r.iy, -r.oy),
+                            fmaxf(__fmaf_rn(nz, r.iz, -r.oz), tmin));
+    const float tf = fmin3f(__fmaf_rn(fx, r.ix, -r.ox), __fmaf_rn(fy, r.iy, -r.oy),
+                            fminf(__fmaf_rn(fz, r.iz, -r.oz), tmax));
+    return tn <= __fmul_rn(tf, 1.0000038f) ? ((__float_as_uint(tn) & ~3u) | slot) : 0xffffffffu;
 }
 
-__device__ __forceinline__ void cswap(float& ta, int32_t& ca, float& tb, int32_t& cb) {
-    const bool s = tb < ta;
-    const float t = ta;
-    const int32_t c = ca;
-    ta = s ? tb : ta;
-    ca = s ? cb : ca;
-    tb = s ? t : tb;
-    cb = s ? c : cb;
+__device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+__device__ __forceinline__ int32_t pick(const int4& c, uint32_t slot) {
+    return slot == 0 ? c.x : slot == 1 ? c.y : slot == 2 ? c.z : c.w;
 }
 
 // Leaf: exact tests of up to 8 consecutive triangles of the leaf-ordered
@@ -247,7 +268,7 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
 // equal t resolves to the lowest triangle id, so the answer is independent of
 // the tree and of the traversal order.  Children are visited
-// nearest-first (4-input sorting network); nodes [0, n_smem) are read from
+// nearest-first (packed-key sorting network); nodes [0, n_smem) are read from
 // the shared-memory copy of the top of the tree.
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
@@ -256,51 +277,54 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            int n_smem = 0) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
-    const float tminf = __double2float_rd(t_min);
+    const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = __double2float_ru(t_max);
     int32_t stack_node[kStackSize];
-    float stack_t[kStackSize];
+    uint32_t stack_key[kStackSize];
     int sp = 0;
     int32_t node = 0;
     for (;;) {
         if (node >= 0) {
-            float4 lx, hx, ly, hy, lz, hz;
+            float4 nx, fx, ny, fy, nz, fz;
             int4 ch;
-            if (node < n_smem) {
+            if (node < n_smem) {   // top of the tree staged in shared memory
                 const float4* q = s_nodes + 8 * node;
-                lx = q[0]; hx = q[1]; ly = q[2]; hy = q[3]; lz = q[4]; hz = q[5];
+                nx = q[r.nx]; fx = q[r.nx ^ 1];
+                ny = q[r.ny]; fy = q[r.ny ^ 1];
+                nz = q[r.nz]; fz = q[r.nz ^ 1];
                 ch = *reinterpret_cast<const int4*>(q + 6);
             } else {
                 const float4* q = reinterpret_cast<const float4*>(nodes + node);
-                lx = __ldg(q + 0); hx = __ldg(q + 1); ly = __ldg(q + 2);
-                hy = __ldg(q + 3); lz = __ldg(q + 4); hz = __ldg(q + 5);
+                nx = __ldg(q + r.nx); fx = __ldg(q + (r.nx ^ 1));
+                ny = __ldg(q + r.ny); fy = __ldg(q + (r.ny ^ 1));
+                nz = __ldg(q + r.nz); fz = __ldg(q + (r.nz ^ 1));
                 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
             }
-            float t0 = ch.x != kEmptyChild ? slab1(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tminf, tb) : INFINITY;
-            float t1 = ch.y != kEmptyChild ? slab1(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tminf, tb) : INFINITY;
-            float t2 = ch.z != kEmptyChild ? slab1(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tminf, tb) : INFINITY;
-            float t3 = ch.w != kEmptyChild ? slab1(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tminf, tb) : INFINITY;
-            int32_t c0 = ch.x, c1 = ch.y, c2 = ch.z, c3 = ch.w;
-            cswap(t0, c0, t1, c1);
-            cswap(t2, c2, t3, c3);
-            cswap(t0, c0, t2, c2);
-            cswap(t1, c1, t3, c3);
-            cswap(t1, c1, t2, c2);
-            if (t3 != INFINITY) { stack_node[sp] = c3; stack_t[sp] = t3; ++sp; }
-            if (t2 != INFINITY) { stack_node[sp] = c2; stack_t[sp] = t2; ++sp; }
-            if (t1 != INFINITY) { stack_node[sp] = c1; stack_t[sp] = t1; ++sp; }
-            if (t0 != INFINITY) {
-                node = c0;
+            uint32_t k0 = slab_key(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tminf, tb, 0u);
+            uint32_t k1 = slab_key(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tminf, tb, 1u);
+            uint32_t k2 = slab_key(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tminf, tb, 2u);
+            uint32_t k3 = slab_key(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tminf, tb, 3u);
+            kswap(k0, k1);
+            kswap(k2, k3);
+            kswap(k0, k2);
+            kswap(k1, k3);
+            kswap(k1, k2);
+            if (k3 != 0xffffffffu) { stack_node[sp] = pick(ch, k3 & 3u); stack_key[sp] = k3; ++sp; }
+            if (k2 != 0xffffffffu) { stack_node[sp] = pick(ch, k2 & 3u); stack_key[sp] = k2; ++sp; }
+            if (k1 != 0xffffffffu) { stack_node[sp] = pick(ch, k1 & 3u); stack_key[sp] = k1; ++sp; }
+            if (k0 != 0xffffffffu) {
+                node = pick(ch, k0 & 3u);
                 continue;
             }
         } else {
             leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb);
         }
-        // pop the next node still in front of the current closest hit
+        // pop the next node still in front of the current closest hit (the
+        // key's t is rounded down, so the cull stays conservative)
         for (;;) {
             if (sp == 0) return h;
             --sp;
-            if (stack_t[sp] <= tb) break;
+            if (__uint_as_float(stack_key[sp] & ~3u) <= tb) break;
         }
         node = stack_node[sp];
     }
