@@ -240,9 +240,7 @@ __device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
 }
 
 __device__ __forceinline__ int32_t pick(const int4& c, uint32_t slot) {
-    const int32_t a = (slot & 1u) ? c.y : c.x;
-    const int32_t b = (slot & 1u) ? c.w : c.z;
-    return (slot & 2u) ? b : a;
+    return slot == 0 ? c.x : slot == 1 ? c.y : slot == 2 ? c.z : c.w;
 }
 
 // Leaf: exact tests of up to 8 consecutive triangles of the leaf-ordered
@@ -330,85 +328,6 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
         }
         node = stack_node[sp];
     }
-}
-
-// Resumable closest-hit query: the same traversal as closest_bvh, split so a
-// caller can advance it one step (node visit or leaf, then pop) at a time.
-struct Trav {
-    RayF r;
-    float tminf, tb;
-    double bt;           // closest t so far (reference-exact)
-    int32_t bid;         // its triangle id, INT32_MAX = none
-    int32_t node;
-    int sp;
-    int32_t sn[kStackSize];
-    uint32_t sk[kStackSize];
-};
-
-__device__ __forceinline__ void trav_init(Trav& T, double ox, double oy, double oz, double dx,
-                                          double dy, double dz, double t_min) {
-    T.r = make_rayf(ox, oy, oz, dx, dy, dz);
-    T.tminf = fmaxf(__double2float_rd(t_min), 0.0f);
-    T.tb = INFINITY;
-    T.bt = INFINITY;
-    T.bid = INT32_MAX;
-    T.node = 0;
-    T.sp = 0;
-}
-
-// One step; returns true when the query has finished (result in bt/bid).
-__device__ __forceinline__ bool trav_step(Trav& T, const GpuNode* __restrict__ nodes,
-                                          const GpuTri* __restrict__ tris, const float4* s_nodes,
-                                          int n_smem, double ox, double oy, double oz, double dx,
-                                          double dy, double dz, double t_min) {
-    if (T.node >= 0) {
-        float4 nx, fx, ny, fy, nz, fz;
-        int4 ch;
-        const RayF& r = T.r;
-        if (T.node < n_smem) {
-            const float4* q = s_nodes + 8 * T.node;
-            nx = q[r.nx]; fx = q[r.nx ^ 1];
-            ny = q[r.ny]; fy = q[r.ny ^ 1];
-            nz = q[r.nz]; fz = q[r.nz ^ 1];
-            ch = *reinterpret_cast<const int4*>(q + 6);
-        } else {
-            const float4* q = reinterpret_cast<const float4*>(nodes + T.node);
-            nx = __ldg(q + r.nx); fx = __ldg(q + (r.nx ^ 1));
-            ny = __ldg(q + r.ny); fy = __ldg(q + (r.ny ^ 1));
-            nz = __ldg(q + r.nz); fz = __ldg(q + (r.nz ^ 1));
-            ch = __ldg(reinterpret_cast<const int4*>(q + 6));
-        }
-        uint32_t k0 = slab_key(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, T.tminf, T.tb, 0u);
-        uint32_t k1 = slab_key(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, T.tminf, T.tb, 1u);
-        uint32_t k2 = slab_key(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, T.tminf, T.tb, 2u);
-        uint32_t k3 = slab_key(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, T.tminf, T.tb, 3u);
-        kswap(k0, k1);
-        kswap(k2, k3);
-        kswap(k0, k2);
-        kswap(k1, k3);
-        kswap(k1, k2);
-        // branch-free pushes (farthest first); the bound max_stack <
-        // kStackSize keeps the unconditional writes in range
-        T.sn[T.sp] = pick(ch, k3 & 3u); T.sk[T.sp] = k3; T.sp += k3 != 0xffffffffu;
-        T.sn[T.sp] = pick(ch, k2 & 3u); T.sk[T.sp] = k2; T.sp += k2 != 0xffffffffu;
-        T.sn[T.sp] = pick(ch, k1 & 3u); T.sk[T.sp] = k1; T.sp += k1 != 0xffffffffu;
-        if (k0 != 0xffffffffu) {
-            T.node = pick(ch, k0 & 3u);
-            return false;
-        }
-    } else {
-        Hit h{T.bt, T.bid};
-        leaf_test(tris, T.node, ox, oy, oz, dx, dy, dz, t_min, h, T.tb);
-        T.bt = h.t;
-        T.bid = h.id;
-    }
-    for (;;) {
-        if (T.sp == 0) return true;
-        --T.sp;
-        if (__uint_as_float(T.sk[T.sp] & ~3u) <= T.tb) break;
-    }
-    T.node = T.sn[T.sp];
-    return false;
 }
 
 // ------------------------------------------------------------------ SH ----

@@ -117,7 +117,7 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
             s->n_nodes = (int64_t)bvh.nodes.size();
             s->max_depth = bvh.max_depth;
             s->max_leaf = bvh.max_leaf;
-            if (bvh.max_stack >= kStackSize) {
+            if (bvh.max_stack > kStackSize) {
                 free_scene(s);
                 return set_error(EF_EUNSUPPORTED, "ef_scene_create: BVH deeper than the traversal stack");
             }

@@ -98,167 +98,9 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats
     ls.sum_t = 0.0;
 }
 
-// Per-path state of the bounce loop.
-template <int NBMAX>
-struct PathState {
-    double ox, oy, oz, dx, dy, dz, plen;
-    float E[NBMAX];
-    uint32_t ray, skey;
-    int src, nrefl, nseg;
-    unsigned long long path, t_start;
-};
-
-template <int NBMAX>
-__device__ __forceinline__ void start_path(const TraceParams& P, PathState<NBMAX>& S,
-                                           unsigned long long path, LaneStats& ls,
-                                           unsigned int* s_stats, double* s_sumt) {
-    S.path = path;
-    S.src = (int)(path / (unsigned long long)P.n_rays);
-    const int64_t local = (int64_t)(path - (unsigned long long)S.src * P.n_rays);
-    S.ray = P.ray_ids ? __ldg(P.ray_ids + local) : P.ray0 + (uint32_t)local;
-    S.skey = P.src_key ? __ldg(P.src_key + S.src) : (uint32_t)S.src;
-    S.ox = __ldg(P.src_pos + 3 * S.src + 0);
-    S.oy = __ldg(P.src_pos + 3 * S.src + 1);
-    S.oz = __ldg(P.src_pos + 3 * S.src + 2);
-    sample_sphere(P.seed, S.skey, S.ray, P.frame, S.dx, S.dy, S.dz);
-#pragma unroll
-    for (int b = 0; b < NBMAX; ++b) S.E[b] = P.e0;
-    S.plen = 0.0;
-    S.nrefl = 0;
-    S.nseg = 0;
-    if (S.src != ls.src) {
-        flush_stats(ls, s_stats, s_sumt);
-        ls.src = S.src;
-    }
-    ls.c[EF_ST_PATHS]++;
-    if (P.timing) S.t_start = globaltimer();
-}
-
-// Everything after the closest hit of one segment: listener-sphere receiver,
-// SH histogram commit, absorption/scattering and the next direction
-// (DESIGN.md 3.3-3.5).  Returns false when the path ends.
-template <int NBMAX, int ORDER>
-__device__ __forceinline__ bool shade(const TraceParams& P, PathState<NBMAX>& S, const Hit& h,
-                                      LaneStats& ls) {
-    constexpr int NK = (ORDER + 1) * (ORDER + 1);
-    const int nb = P.nb;
-    const bool hit = h.id != INT32_MAX;
-    if (P.path_ids && !P.timing) P.path_ids[S.path * P.max_bounces + S.nseg] = hit ? h.id : -1;
-    {
-        const double Lx = P.lx - S.ox, Ly = P.ly - S.oy, Lz = P.lz - S.oz;
-        const double tc = dot3(Lx, Ly, Lz, S.dx, S.dy, S.dz);
-        const double tlim = hit ? h.t : INFINITY;
-        if (tc > 0.0 && tc < tlim) {
-            const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
-            const double perp2 = dist2 - tc * tc;
-            if (perp2 <= P.r2) {
-                float* dst = nullptr;
-                ls.c[EF_ST_ARRIVALS]++;
-                if (S.nrefl == 0) {
-                    ls.c[EF_ST_DIRECT]++;
-                    dst = P.Dir + (size_t)S.src * nb * NK;
-                } else {
-                    const double q = (S.plen + tc) / P.bin_len;
-                    if (q < (double)P.n_bins)
-                        dst = P.H + ((size_t)S.src * P.n_bins + (size_t)q) * nb * NK;
-                    else
-                        ls.c[EF_ST_DROPPED]++;
-                }
-                if (dst) {
-                    double Y[NK];
-                    eval_sh<ORDER>(-S.dx, -S.dy, -S.dz, Y);
-                    float Yf[NK];
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
-#pragma unroll
-                    for (int b = 0; b < NBMAX; ++b) {
-                        if (b < nb) {
-#pragma unroll
-                            for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, S.E[b] * Yf[k]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-    ++S.nseg;
-    ls.c[EF_ST_SEGMENTS]++;
-    bool alive = true;
-    if (!hit) {
-        ls.c[EF_ST_ESCAPED]++;
-        alive = false;
-    } else {
-        const double t = h.t;
-        S.plen += t;
-        ls.sum_t += t;
-        S.ox = S.ox + t * S.dx;
-        S.oy = S.oy + t * S.dy;
-        S.oz = S.oz + t * S.dz;
-        ++S.nrefl;
-        ls.c[EF_ST_REFLECTIONS]++;
-        const int m = __ldg(P.mat + h.id);
-        const double nx = __ldg(P.normals + 3 * h.id + 0);
-        const double ny = __ldg(P.normals + 3 * h.id + 1);
-        const double nz = __ldg(P.normals + 3 * h.id + 2);
-        double u1, u2;
-        draw2(S.ray, (uint32_t)S.nrefl, 0u, P.frame, P.seed, S.skey, u1, u2);
-        const bool diffuse = u1 < __ldg(P.pdiff + m);
-        const float* f = (diffuse ? P.fd : P.fs) + m * nb;
-#pragma unroll
-        for (int b = 0; b < NBMAX; ++b)
-            if (b < nb) S.E[b] = S.E[b] * __ldg(f + b);
-        const double nd = dot3(nx, ny, nz, S.dx, S.dy, S.dz);
-        if (diffuse) {
-            const double sgn = nd > 0.0 ? -1.0 : 1.0;
-            sample_cosine(P.seed, S.skey, S.ray, (uint32_t)S.nrefl, P.frame, sgn * nx, sgn * ny,
-                          sgn * nz, S.dx, S.dy, S.dz);
-        } else {
-            const double k2 = 2.0 * nd;
-            S.dx = S.dx - k2 * nx;
-            S.dy = S.dy - k2 * ny;
-            S.dz = S.dz - k2 * nz;
-        }
-        if (S.nrefl >= P.max_bounces) alive = false;
-    }
-    if (!alive) {
-        if (P.path_nseg) P.path_nseg[S.path] = S.nseg;
-        if (P.timing) {
-            const unsigned long long t_end = globaltimer();
-            int32_t* row = P.path_ids + S.path * P.max_bounces;
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            row[0] = (int32_t)(S.t_start & 0xffffffffu);
-            row[1] = (int32_t)(S.t_start >> 32);
-            row[2] = (int32_t)(t_end & 0xffffffffu);
-            row[3] = (int32_t)(t_end >> 32);
-            row[4] = (int32_t)smid;
-            row[5] = S.nseg;
-        }
-    }
-    return alive;
-}
-
-// Warp-aggregated path fetch: idle lanes take consecutive path indices.
-__device__ __forceinline__ bool fetch_path(const TraceParams& P, bool need, int lane,
-                                           unsigned long long& path) {
-    const unsigned mask = __ballot_sync(kFull, need);
-    if (!mask) return false;
-    const int leader = __ffs(mask) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(P.counter, (unsigned long long)__popc(mask));
-    base = __shfl_sync(kFull, base, leader);
-    if (!need) return false;
-    path = base + __popc(mask & ((1u << lane) - 1u));
-    return path < P.total;
-}
-
-// The persistent trace megakernel.  BVH mode runs a per-lane state machine:
-// every iteration each lane performs ONE traversal step (a 4-wide node visit
-// or a leaf test, then a pop); a lane whose query finished shades its segment
-// and starts the next one (or fetches a new path) in the same iteration, so
-// no lane idles while its warp-mates finish longer traversals.
 template <int NBMAX, int ORDER, bool BRUTE>
 __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TraceParams P) {
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
     extern __shared__ __align__(16) unsigned char smem[];
     // per-block counters: f64 path-length sums, then u32 counters (a block's
     // per-source counts stay far below 2^32), then the all-pairs triangles
@@ -280,46 +122,157 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
+    const int nb = P.nb;
     LaneStats ls;
-    PathState<NBMAX> S;
-    S.t_start = 0;
     bool active = false, exhausted = false;
+    double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 1, plen = 0;
+    float E[NBMAX];
+#pragma unroll
+    for (int b = 0; b < NBMAX; ++b) E[b] = 0.f;
+    uint32_t ray = 0, skey = 0;
+    int src = 0, nrefl = 0, nseg = 0;
+    unsigned long long path = 0;
+    unsigned long long t_start = 0;
 
-    if constexpr (BRUTE) {
-        for (;;) {
-            unsigned long long path = 0;
-            const bool need = !active && !exhausted;
-            if (fetch_path(P, need, lane, path)) {
-                start_path(P, S, path, ls, s_stats, s_sumt);
-                active = true;
-            } else if (need) {
-                exhausted = true;
+    for (;;) {
+        // ---- warp-aggregated refill: idle lanes take the next path indices
+        const bool need = !active && !exhausted;
+        const unsigned mask = __ballot_sync(kFull, need);
+        if (mask) {
+            const int leader = __ffs(mask) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(P.counter, (unsigned long long)__popc(mask));
+            base = __shfl_sync(kFull, base, leader);
+            if (need) {
+                path = base + __popc(mask & ((1u << lane) - 1u));
+                if (path >= P.total) {
+                    exhausted = true;
+                } else {
+                    src = (int)(path / (unsigned long long)P.n_rays);
+                    const int64_t local = (int64_t)(path - (unsigned long long)src * P.n_rays);
+                    ray = P.ray_ids ? __ldg(P.ray_ids + local) : P.ray0 + (uint32_t)local;
+                    skey = P.src_key ? __ldg(P.src_key + src) : (uint32_t)src;
+                    ox = __ldg(P.src_pos + 3 * src + 0);
+                    oy = __ldg(P.src_pos + 3 * src + 1);
+                    oz = __ldg(P.src_pos + 3 * src + 2);
+                    sample_sphere(P.seed, skey, ray, P.frame, dx, dy, dz);
+#pragma unroll
+                    for (int b = 0; b < NBMAX; ++b) E[b] = P.e0;
+                    plen = 0.0;
+                    nrefl = 0;
+                    nseg = 0;
+                    if (src != ls.src) {
+                        flush_stats(ls, s_stats, s_sumt);
+                        ls.src = src;
+                    }
+                    ls.c[EF_ST_PATHS]++;
+                    if (P.timing) t_start = globaltimer();
+                    active = true;
+                }
             }
-            if (__all_sync(kFull, !active)) break;
-            if (!active) continue;
-            const Hit h = closest_brute(s_tri, P.n_tri, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps,
-                                        INFINITY);
-            active = shade<NBMAX, ORDER>(P, S, h, ls);
         }
-    } else {
-        Trav T;
-        for (;;) {
-            unsigned long long path = 0;
-            const bool need = !active && !exhausted;
-            if (fetch_path(P, need, lane, path)) {
-                start_path(P, S, path, ls, s_stats, s_sumt);
-                trav_init(T, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps);
-                active = true;
-            } else if (need) {
-                exhausted = true;
+        if (__all_sync(kFull, !active)) break;
+        if (!active) continue;
+
+        // ---- closest hit (exact f64 leaf test)
+        Hit h;
+        if (BRUTE)
+            h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+        else
+            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
+                                P.n_smem_nodes);
+        const bool hit = h.id != INT32_MAX;
+        if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
+
+        // ---- listener sphere receiver + SH histogram commit
+        {
+            const double Lx = P.lx - ox, Ly = P.ly - oy, Lz = P.lz - oz;
+            const double tc = dot3(Lx, Ly, Lz, dx, dy, dz);
+            const double tlim = hit ? h.t : INFINITY;
+            if (tc > 0.0 && tc < tlim) {
+                const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
+                const double perp2 = dist2 - tc * tc;
+                if (perp2 <= P.r2) {
+                    float* dst = nullptr;
+                    ls.c[EF_ST_ARRIVALS]++;
+                    if (nrefl == 0) {
+                        ls.c[EF_ST_DIRECT]++;
+                        dst = P.Dir + (size_t)src * nb * NK;
+                    } else {
+                        const double q = (plen + tc) / P.bin_len;
+                        if (q < (double)P.n_bins)
+                            dst = P.H + ((size_t)src * P.n_bins + (size_t)q) * nb * NK;
+                        else
+                            ls.c[EF_ST_DROPPED]++;
+                    }
+                    if (dst) {
+                        double Y[NK];
+                        eval_sh<ORDER>(-dx, -dy, -dz, Y);
+                        float Yf[NK];
+#pragma unroll
+                        for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
+#pragma unroll
+                        for (int b = 0; b < NBMAX; ++b) {
+                            if (b < nb) {
+#pragma unroll
+                                for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, E[b] * Yf[k]);
+                            }
+                        }
+                    }
+                }
             }
-            if (__all_sync(kFull, !active)) break;
-            if (!active) continue;
-            if (trav_step(T, P.nodes, P.tris, s_nodes, P.n_smem_nodes, S.ox, S.oy, S.oz, S.dx, S.dy,
-                          S.dz, kRayEps)) {
-                active = shade<NBMAX, ORDER>(P, S, Hit{T.bt, T.bid}, ls);
-                if (active) trav_init(T, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps);
+        }
+        ++nseg;
+        ls.c[EF_ST_SEGMENTS]++;
+        if (!hit) {
+            ls.c[EF_ST_ESCAPED]++;
+            active = false;
+        } else {
+            // ---- reflection
+            const double t = h.t;
+            plen += t;
+            ls.sum_t += t;
+            ox = ox + t * dx;
+            oy = oy + t * dy;
+            oz = oz + t * dz;
+            ++nrefl;
+            ls.c[EF_ST_REFLECTIONS]++;
+            const int m = __ldg(P.mat + h.id);
+            const double nx = __ldg(P.normals + 3 * h.id + 0);
+            const double ny = __ldg(P.normals + 3 * h.id + 1);
+            const double nz = __ldg(P.normals + 3 * h.id + 2);
+            double u1, u2;
+            draw2(ray, (uint32_t)nrefl, 0u, P.frame, P.seed, skey, u1, u2);
+            const bool diffuse = u1 < __ldg(P.pdiff + m);
+            const float* f = (diffuse ? P.fd : P.fs) + m * nb;
+#pragma unroll
+            for (int b = 0; b < NBMAX; ++b)
+                if (b < nb) E[b] = E[b] * __ldg(f + b);
+            const double nd = dot3(nx, ny, nz, dx, dy, dz);
+            if (diffuse) {
+                const double s = nd > 0.0 ? -1.0 : 1.0;
+                sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny, s * nz,
+                              dx, dy, dz);
+            } else {
+                const double k2 = 2.0 * nd;
+                dx = dx - k2 * nx;
+                dy = dy - k2 * ny;
+                dz = dz - k2 * nz;
             }
+            if (nrefl >= P.max_bounces) active = false;
+        }
+        if (!active && P.path_nseg) P.path_nseg[path] = nseg;
+        if (!active && P.timing) {
+            const unsigned long long t_end = globaltimer();
+            int32_t* row = P.path_ids + path * P.max_bounces;
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            row[0] = (int32_t)(t_start & 0xffffffffu);
+            row[1] = (int32_t)(t_start >> 32);
+            row[2] = (int32_t)(t_end & 0xffffffffu);
+            row[3] = (int32_t)(t_end >> 32);
+            row[4] = (int32_t)smid;
+            row[5] = nseg;
         }
     }
     flush_stats(ls, s_stats, s_sumt);
