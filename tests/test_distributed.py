@@ -1,0 +1,76 @@
+"""Multi-rank path on CPU (gloo, world size 2): ray shards traced by the
+oracle on each rank and reduce-scattered with the product's helper equal the
+unsharded frame (counts exactly, histograms to f64 rounding)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_frame(w, src_ids, ray0, n):
+    from oracle import oracle as O
+    os_ = O.OracleScene.from_arrays(w.arrays())
+    H, stats = [], []
+    for s in src_ids:
+        r = O.trace(os_, src_key=s, src_pos=w.sources[s], listener=w.listener, radius=w.radius,
+                    seed=w.seed, order=w.order, n_bins=w.n_bins, bin_len=w.speed_of_sound * w.bin_s,
+                    max_bounces=w.max_bounces, e0=1.0, ray0=ray0, n_rays=n)
+        H.append(r.H)
+        stats.append([r.stats["segments"], r.stats["arrivals"], r.stats["reflections"]])
+    return np.array(H), np.array(stats, dtype=np.float64)
+
+
+def _worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1803_00430_b200 import distributed, workloads
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = workloads.c1_shoebox()
+    w.sources = np.array([[2.0, 2.0, 1.5], [3.0, 6.0, 1.0]])
+    ray0, nr = distributed.shard_rays(n, rank)
+    H, st = _oracle_frame(w, [0, 1], ray0, nr)
+    Hr = distributed.reduce_scatter_sources(torch.from_numpy(H))
+    Sr = distributed.reduce_scatter_sources(torch.from_numpy(st))
+    q.put((rank, Hr.numpy(), Sr.numpy()))
+    dist.destroy_process_group()
+
+
+def test_sharded_frame_equals_unsharded():
+    from paper_1803_00430_b200 import workloads
+    world, n = 2, 512
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (h, s)) for r, h, s in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = workloads.c1_shoebox()
+    w.sources = np.array([[2.0, 2.0, 1.5], [3.0, 6.0, 1.0]])
+    H, st = _oracle_frame(w, [0, 1], 0, world * n)
+    for r in range(world):
+        h, s = res[r]
+        assert np.array_equal(s[0], st[r])                     # exact counts
+        np.testing.assert_allclose(h[0], H[r], rtol=1e-12, atol=1e-18)
+
+
+def test_owned_sources_validation():
+    from paper_1803_00430_b200 import distributed
+    assert distributed.owned_sources(8, 1, 4) == slice(2, 4)
+    with pytest.raises(ValueError):
+        distributed.owned_sources(7, 0, 2)

@@ -1,0 +1,87 @@
+"""Summarise an ncu launch list and a full capture into profiles/.
+
+    python tools/summarize_ncu.py gpurun_out/launches.csv gpurun_out/prof_trace.ncu-rep profiles/r01_c2
+
+Writes <prefix>_launches.txt (per-kernel device time, share of the step),
+<prefix>_trace_full.txt (key metrics of the captured kernel) and
+profiles/traffic_<config>.json (DRAM bytes per launch, read by bench.py)."""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+        "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "smsp__inst_executed.sum", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "sm__cycles_active.avg", "gpc__cycles_elapsed.max",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    d = collections.defaultdict(list)
+    for r in rows[h + 1:]:
+        try:
+            d[r[4]].append(float(r[-1].replace(",", "")))
+        except (ValueError, IndexError):
+            pass
+    return d
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {k: (vals[hdr.index(k)], units[hdr.index(k)]) for k in KEYS if k in hdr}, vals[hdr.index("Kernel Name")]
+
+
+def main():
+    lpath, rep, prefix = sys.argv[1:4]
+    config = sys.argv[4] if len(sys.argv) > 4 else "c2"
+    d = launches(lpath)
+    tot = sum(sum(v) / len(v) for k, v in d.items() if "ef::" in k)
+    lines = ["kernel | launches | mean device time (us) | share of the library's step time",
+             "---|---|---|---"]
+    for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
+        m = sum(v) / len(v) / 1e3
+        share = f"{100 * m * 1e3 / tot:.1f}%" if "ef::" in k else "(torch / bench plumbing)"
+        lines.append(f"{k[:70]} | {len(v)} | {m:.1f} | {share}")
+    open(prefix + "_launches.txt", "w").write(
+        "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n"
+        + "\n".join(lines) + "\n")
+    m, name = raw(rep)
+    body = [f"# ncu --set full --clock-control none, kernel: {name}"]
+    for k in KEYS:
+        if k in m:
+            body.append(f"{k} = {m[k][0]} {m[k][1]}")
+    open(prefix + "_trace_full.txt", "w").write("\n".join(body) + "\n")
+    rd = float(m["dram__bytes_read.sum"][0].replace(",", ""))
+    wr = float(m["dram__bytes_write.sum"][0].replace(",", ""))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd *= scale.get(m["dram__bytes_read.sum"][1], 1)
+    wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
+    os.makedirs("profiles", exist_ok=True)
+    json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": rep,
+               "note": "one ncu --set full capture of trace_kernel"},
+              open(os.path.join("profiles", f"traffic_{config}.json"), "w"), indent=1)
+    print("\n".join(lines))
+    print("\n".join(body))
+
+
+if __name__ == "__main__":
+    main()
