@@ -47,7 +47,9 @@ enum {
     EF_ST_DIRECT,          /* crossings before any reflection (-> Dir)          */
     EF_ST_DROPPED,         /* late arrivals past the IR length    */
     EF_ST_ESCAPED,         /* paths that left the scene                         */
-    EF_ST_COUNT = 8
+    EF_ST_NODES,           /* BVH nodes visited (device tree)                   */
+    EF_ST_TRIS,            /* exact triangle tests (device tree / all-pairs)    */
+    EF_ST_COUNT = 10
 };
 
 /* Per-(source, band) analysis outputs (f64), index into params. */

@@ -16,8 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libechoforge_b200.so")
 
 EF_OK, EF_EINVAL, EF_ECUDA, EF_ENOMEM, EF_EUNSUPPORTED = 0, -1, -2, -3, -4
-ST_NAMES = ("paths", "segments", "reflections", "arrivals", "direct", "dropped", "escaped")
-EF_ST_COUNT = 8
+ST_NAMES = ("paths", "segments", "reflections", "arrivals", "direct", "dropped", "escaped",
+            "nodes", "tris")
+EF_ST_COUNT = 10
 P_NAMES = ("rt60", "gain", "drr_db", "total", "direct", "silent", "fit_n", "slope",
            "first_bin", "last_bin")
 EF_P_COUNT = 10

@@ -11,6 +11,7 @@
 // structure-of-arrays) numbered depth-first for locality.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -50,7 +51,17 @@ struct BNode {
 
 constexpr int kBins = 32;
 constexpr double kTraverseCost = 1.0;
-constexpr double kIntersectCost = 2.0;   // f64 Moeller-Trumbore vs an f32 box pair
+// f64 Moeller-Trumbore vs an f32 box test; EF_BVH_CI / EF_BVH_MAXLEAF override
+// (tuning experiments only)
+double intersect_cost() {
+    const char* e = std::getenv("EF_BVH_CI");
+    return e ? std::atof(e) : 2.0;
+}
+int max_leaf() {
+    const char* e = std::getenv("EF_BVH_MAXLEAF");
+    const int v = e ? std::atoi(e) : kMaxLeaf;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+}
 constexpr int kForceMedianDepth = 32;
 
 struct Builder {
@@ -60,6 +71,8 @@ struct Builder {
     std::vector<BNode> nodes;
     int max_depth = 0;
     int max_leaf = 0;
+    const double kIntersectCost = intersect_cost();
+    const int kLeafMax = ef::max_leaf();
 
     Builder(const std::vector<Box>& b, const std::vector<double>& c, std::vector<int64_t>& i)
         : tb(b), cen(c), idx(i) {}
@@ -124,7 +137,7 @@ struct Builder {
                 }
             }
             double leaf_cost = kIntersectCost * (double)n;
-            if (n <= kMaxLeaf && (best_axis < 0 || leaf_cost <= best)) return make_leaf(box, s, n);
+            if (n <= kLeafMax && (best_axis < 0 || leaf_cost <= best)) return make_leaf(box, s, n);
             if (best_axis >= 0) {
                 double scale = kBins / (cbox.hi[best_axis] - cbox.lo[best_axis]);
                 auto it = std::partition(idx.begin() + s, idx.begin() + e, [&](int64_t t) {
@@ -135,7 +148,7 @@ struct Builder {
                 mid = it - idx.begin();
                 split_found = mid > s && mid < e;
             }
-        } else if (n <= kMaxLeaf) {
+        } else if (n <= kLeafMax) {
             return make_leaf(box, s, n);
         }
         if (!split_found) {

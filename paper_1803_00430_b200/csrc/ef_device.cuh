@@ -247,9 +247,10 @@ __device__ __forceinline__ int32_t pick(const int4& c, uint32_t slot) {
 // payload; equal t resolves to the lowest original id.
 __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32_t enc, double ox,
                                           double oy, double oz, double dx, double dy, double dz,
-                                          double t_min, Hit& h, float& tb) {
+                                          double t_min, Hit& h, float& tb, uint32_t& n_tris) {
     const uint32_t e = ~(uint32_t)enc;
     const uint32_t start = e >> 3, cnt = (e & 7u) + 1u;
+    n_tris += cnt;
     for (uint32_t i = 0; i < cnt; ++i) {
         const double2* q = reinterpret_cast<const double2*>(tris + start + i);
         const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3),
@@ -273,8 +274,8 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
-                                           double t_max, const float4* s_nodes = nullptr,
-                                           int n_smem = 0) {
+                                           double t_max, const float4* s_nodes, int n_smem,
+                                           uint32_t& n_nodes, uint32_t& n_tris) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
@@ -285,6 +286,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     int32_t node = 0;
     for (;;) {
         if (node >= 0) {
+            ++n_nodes;
             float4 nx, fx, ny, fy, nz, fz;
             int4 ch;
             if (node < n_smem) {   // top of the tree staged in shared memory
@@ -317,7 +319,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                 continue;
             }
         } else {
-            leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb);
+            leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
         }
         // pop the next node still in front of the current closest hit (the
         // key's t is rounded down, so the cull stays conservative)
@@ -328,6 +330,14 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
         }
         node = stack_node[sp];
     }
+}
+
+__device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
+                                           const GpuTri* __restrict__ tris, double ox, double oy,
+                                           double oz, double dx, double dy, double dz, double t_min,
+                                           double t_max) {
+    uint32_t a = 0, b = 0;
+    return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, nullptr, 0, a, b);
 }
 
 // ------------------------------------------------------------------ SH ----

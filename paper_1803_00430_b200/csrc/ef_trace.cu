@@ -176,11 +176,13 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
 
         // ---- closest hit (exact f64 leaf test)
         Hit h;
-        if (BRUTE)
+        if (BRUTE) {
             h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+            ls.c[EF_ST_TRIS] += P.n_tri;
+        }
         else
             h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
-                                P.n_smem_nodes);
+                            P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS]);
         const bool hit = h.id != INT32_MAX;
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 

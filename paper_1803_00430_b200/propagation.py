@@ -85,6 +85,8 @@ class TraceStats:
     dropped_late: int = 0
     escaped: int = 0
     open_field: bool = False
+    nodes_visited: int = 0        # device BVH work (not the reference's)
+    triangles_tested: int = 0
 
 
 @dataclass
@@ -106,11 +108,11 @@ class CoherenceCaches:
 
 
 def _stats_from_row(row: np.ndarray, sum_t: float) -> TraceStats:
-    paths, segs, refl, arr, direct, dropped, esc = (int(x) for x in row[:7])
+    paths, segs, refl, arr, direct, dropped, esc, nodes, tris = (int(x) for x in row[:9])
     return TraceStats(mean_free_path=sum_t / refl if refl else 0.0,
                       primary_rays_emitted=paths, total_segments=segs, reflections=refl,
                       arrivals=arr, direct_arrivals=direct, dropped_late=dropped, escaped=esc,
-                      open_field=refl == 0)
+                      open_field=refl == 0, nodes_visited=nodes, triangles_tested=tris)
 
 
 class FrameTracer:

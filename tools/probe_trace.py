@@ -113,3 +113,33 @@ def single(name="c2", src=6, ray=27707, reps=5):
 
 if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "single":
     single(sys.argv[1])
+
+
+def knobs(name="c2"):
+    """Frame time and device work per segment for the current EF_BVH_* knobs."""
+    w = workloads.WORKLOADS[name]()
+    sc = scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = propagation.FrameTracer(sc, len(w.sources), cfg)
+    tr.set_sources(w.sources)
+    ms, segs = time_trace(tr, w)
+    st = tr.stats.sum(0).cpu().numpy()
+    info = sc.device_info()
+    print(f"[{name}] CI={os.environ.get('EF_BVH_CI', '2')} LEAF={os.environ.get('EF_BVH_MAXLEAF', '4')} "
+          f"nodes={info['n_nodes']} depth={info['max_depth']} leafmax={info['max_leaf']}: "
+          f"{ms*1e3:.1f} us  nodes/seg {st[7]/st[1]:.2f} tris/seg {st[8]/st[1]:.2f}")
+    tr1 = propagation.FrameTracer(sc, 1, cfg, record=2)
+    tr1.set_sources(w.sources[6:7], [6])
+    tr1.trace(w.listener, ray_ids=[27707])
+    torch.cuda.synchronize()
+    r = tr1.path_ids.cpu().numpy().reshape(-1)[:6].astype(np.int64)
+    t0 = (r[0] & 0xffffffff) | (r[1] << 32)
+    t1 = (r[2] & 0xffffffff) | (r[3] << 32)
+    st1 = tr1.stats.sum(0).cpu().numpy()
+    print(f"    single long path: {(t1 - t0) / 1e3 / r[5]:.2f} us/seg, nodes/seg {st1[7]/st1[1]:.2f} "
+          f"tris/seg {st1[8]/st1[1]:.2f}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "knobs":
+    knobs(sys.argv[1])
