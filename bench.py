@@ -38,6 +38,9 @@ sys.path.insert(0, ROOT)
 WORK = {
     "c1": dict(N_node=0.0, N_tri=12.0, P_arr=0.011300),
     "c2": dict(N_node=32.304, N_tri=5.334, P_arr=0.0),
+    # subsampled (tools/measure_work.py c3 2048 8 / c5 1024 16)
+    "c3": dict(N_node=74.351, N_tri=12.123, P_arr=0.001952),
+    "c5": dict(N_node=66.946, N_tri=7.966, P_arr=0.0),
 }
 
 
@@ -217,14 +220,28 @@ def run_gpu(args, w, metric, unit):
     stream = torch.cuda.current_stream()
     total_rays = w.n_rays * world
     ray0 = rank * w.n_rays
-
-    k_start = torch.cuda.Event(enable_timing=True)
-    k_end = torch.cuda.Event(enable_timing=True)
+    # C3: moving sources, temporal IR cache (accumulate_ir, tau_LR = 3 s) and
+    # per-frame estimation on the cached IR
+    dynamic = w.n_frames > 1 and w.source_velocity is not None
+    if dynamic:
+        from paper_1803_00430_b200.analysis import blend_into
+        from paper_1803_00430_b200.propagation import TAU_LR
+        pos_all = torch.tensor(np.stack([w.source_positions(f) for f in range(w.n_frames)]),
+                               dtype=torch.float64, device=dev)
+        alpha = 1.0 - float(np.exp(-w.frame_dt / TAU_LR))
+        H_cache = torch.zeros_like(H_own if world > 1 else tr.H)
+        D_cache = torch.zeros_like(D_own if world > 1 else tr.Dir)
+    seg_total = torch.zeros((), dtype=torch.int64, device=dev)
+    counter = [0]
 
     def step(kernel_events=None):
+        f = counter[0] % max(w.n_frames, 1)
+        counter[0] += 1
+        if dynamic:
+            tr.src_pos.copy_(pos_all[f])
         if kernel_events:
             kernel_events[0].record(stream)
-        tr.trace(w.listener, ray0=ray0, total_rays=total_rays)
+        tr.trace(w.listener, frame=f, ray0=ray0, total_rays=total_rays)
         if kernel_events:
             kernel_events[1].record(stream)
         if world > 1:
@@ -232,14 +249,18 @@ def run_gpu(args, w, metric, unit):
             dist.reduce_scatter_tensor(D_own, tr.Dir)
             dist.reduce_scatter_tensor(st_own, tr.stats)
             dist.reduce_scatter_tensor(su_own, tr.sum_t)
-            an.run(H_own, D_own, st_own, su_own)
+            hs, ds, sts, sus = H_own, D_own, st_own, su_own
         else:
-            an.run(tr.H, tr.Dir, tr.stats, tr.sum_t)
+            hs, ds, sts, sus = tr.H, tr.Dir, tr.stats, tr.sum_t
+        if dynamic:
+            blend_into(H_cache, hs, alpha)
+            blend_into(D_cache, ds, alpha)
+            hs, ds = H_cache, D_cache
+        an.run(hs, ds, sts, sus)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    segs_per_step = int(tr.stats[:, 1].sum().item())   # this rank's segments (deterministic)
     arrivals = int(tr.stats[:, 3].sum().item())
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -256,14 +277,14 @@ def run_gpu(args, w, metric, unit):
             starts[i].record(stream)
             step(kev[i])
             ends[i].record(stream)
+            seg_total.add_(tr.stats[:, 1].sum())     # after the end event: not timed
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     n_launch = _lib.launch_count() - n_launch0
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     k_ms = sum(a.elapsed_time(b) for a, b in kev)
-    segs_check = int(tr.stats[:, 1].sum().item())
-    assert segs_check == segs_per_step, "segment count changed between steps"
+    segs_per_step = int(seg_total.item()) / args.steps   # this rank's mean segments per frame
 
     # ---- e2e through the public API: pinned host in/out, copies timed
     src_host = torch.from_numpy(np.ascontiguousarray(w.sources, np.float64)).pin_memory()
@@ -286,12 +307,12 @@ def run_gpu(args, w, metric, unit):
 
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, k_ms, e_ms], dtype=torch.float64, device=dev)
-    segs = torch.tensor([segs_per_step], dtype=torch.float64, device=dev)
+    segs = torch.tensor([float(seg_total.item())], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(segs, op=dist.ReduceOp.SUM)
     ms, k_ms, e_ms = (float(x) for x in t.cpu())
-    total_segs = float(segs.item()) * args.steps
+    total_segs = float(segs.item())
     value = total_segs / (ms * 1e-3)
     e2e_value = total_segs / (e_ms * 1e-3)
 
@@ -318,7 +339,7 @@ def run_gpu(args, w, metric, unit):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "trace_kernel", "kernel_ms_per_launch": avg_k_s * 1e3,
                          "algorithmic_bytes_per_segment": bseg,
-                         "segments_per_launch": segs_per_step},
+                         "segments_per_launch": round(segs_per_step)},
             "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
             "clocks": clocks.summary()}
     if world == 1 and not args.no_cpu_baseline:
@@ -341,8 +362,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(WORK))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-fraction", type=float, default=1.0,
-                    help="fraction of each source's rays in the CPU sample")
+    ap.add_argument("--cpu-fraction", type=float, default=None,
+                    help="fraction of each source's rays in the CPU sample (default per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum wall time of the CPU baseline sample")
@@ -350,6 +371,8 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1803_00430_b200 import workloads
     w = workloads.WORKLOADS[args.config]()
+    if args.cpu_fraction is None:
+        args.cpu_fraction = {"c1": 1.0, "c2": 1.0, "c3": 1.0 / 32, "c5": 1.0 / 1024}[args.config]
     metric = "ray-bounce segments/sec into SH energy IRs"
     unit = "segments/s"
     if args.impl == "reference":

@@ -147,3 +147,12 @@ def blend_histograms(cache, frame, alpha: float):
     _lib.check(_lib.lib().ef_blend(_lib.ptr(cache.contiguous()), _lib.ptr(frame.contiguous()),
                                    frame.numel(), float(alpha), _lib.ptr(out), _lib.stream_handle()))
     return out
+
+
+def blend_into(cache, frame, alpha: float):
+    """In-place cache <- a*frame + (1-a)*cache on the device."""
+    if cache.shape != frame.shape or not cache.is_contiguous() or not frame.is_contiguous():
+        raise ValueError("cache and frame must be contiguous tensors of one shape")
+    _lib.check(_lib.lib().ef_blend(_lib.ptr(cache), _lib.ptr(frame), frame.numel(), float(alpha),
+                                   _lib.ptr(cache), _lib.stream_handle()))
+    return cache

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     }
 }
 
-__global__ void blend_kernel(const float* __restrict__ cache, const float* __restrict__ frame,
+__global__ void blend_kernel(const float* cache, const float* frame,
                              int64_t n, float a, float b, float* out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)

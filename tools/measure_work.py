@@ -22,12 +22,13 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     w = workloads.WORKLOADS[name]()
     n = int(sys.argv[2]) if len(sys.argv) > 2 else w.n_rays
+    n_src = int(sys.argv[3]) if len(sys.argv) > 3 else len(w.sources)
     t0 = time.time()
     os_ = O.OracleScene.from_arrays(w.arrays())
     build = time.time() - t0
     tot = dict.fromkeys(O.ST_NAMES, 0)
     t0 = time.time()
-    for s in range(len(w.sources)):
+    for s in range(n_src):
         r = O.trace(os_, src_key=s, src_pos=w.sources[s], listener=w.listener, radius=w.radius,
                     seed=w.seed, order=w.order, n_bins=w.n_bins, bin_len=w.speed_of_sound * w.bin_s,
                     max_bounces=w.max_bounces, e0=1.0, n_rays=n)
@@ -41,7 +42,7 @@ def main():
     p_arr = tot["arrivals"] / seg
     b_seg = 72 * n_tri + 32 * n_node + (28 + 8 * nb) + p_arr * 8 * nb * nk
     print(json.dumps(dict(config=name, n_tri_scene=w.n_tri, rays_per_source=n,
-                          sources=len(w.sources), seg_per_path=seg / tot["paths"],
+                          sources=n_src, seg_per_path=seg / tot["paths"],
                           N_node=round(n_node, 3), N_tri=round(n_tri, 3), P_arr=p_arr,
                           B_seg=round(b_seg, 1), oracle_build_s=round(build, 2),
                           oracle_seg_per_s_1thread=round(seg / dt), **tot)))
