@@ -202,6 +202,36 @@ int ef_analyze(const ef_analysis_config* cfg, const float* H, const float* Dir,
 int ef_blend(const float* cache, const float* frame, int64_t n, double alpha, float* out,
              void* stream);
 
+/* ---- SH-domain auralization (BASELINE config C4) ---------------------
+ * Replaces the SPEC-only reverb renderer (C4's 16-line FDN
+ * per band) and spatialize_hrtf.  Semantics: DESIGN.md 3.7.
+ * ef_audio_create takes HOST parameter arrays (copied):
+ *   sos (4 bands, 5 biquads, b0 b1 b2 a1 a2) f32; Y (S,16) f32 direct SH
+ *   encoding; d_int/d_w (S) direct delay = d_int + 1 - d_w samples; gain (S,4)
+ *   direct gain per band; p_int/p_w (S) predelay likewise; fdn_delay (S,16)
+ *   i32 line delays in (512, line_len]; g_line (S,4,16) f32 line gains;
+ *   M (S,4,16,16) f32 line -> SH matrices; hrtf_spec (16,2,513) complex f32
+ *   rFFT(1024) of the zero-padded 2-ear filters.
+ * ef_audio_process renders one 512-sample block: x (S,512) f32 DEVICE input,
+ * bus_out (16,512) f32 DEVICE or NULL, out (2,512) f32 DEVICE binaural. */
+typedef struct {
+    int32_t n_sources;
+    int32_t hist_len;   /* band history ring length, power of two       */
+    int32_t line_len;   /* FDN line ring length, power of two            */
+    int32_t reserved;
+} ef_audio_config;
+
+typedef struct ef_audio ef_audio;
+
+int ef_audio_create(const ef_audio_config* cfg, const float* sos, const float* Y,
+                    const int32_t* d_int, const float* d_w, const float* gain,
+                    const int32_t* p_int, const float* p_w, const int32_t* fdn_delay,
+                    const float* g_line, const float* M, const float* hrtf_spec, ef_audio** out);
+int ef_audio_destroy(ef_audio* audio);
+/* out[0]=n_sources out[1]=device bytes out[2]=next sample index out[3]=grid */
+int ef_audio_info(const ef_audio* audio, int64_t* out4);
+int ef_audio_process(ef_audio* audio, const float* x, float* bus_out, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

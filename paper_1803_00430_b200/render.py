@@ -1,0 +1,121 @@
+"""SH-domain auralization on the B200 (BASELINE config C4).
+
+``SHRenderer(params)`` uploads per-source parameters once; ``process(x)``
+renders one 512-sample block for every source: LR4 crossover into band
+histories, direct tap + order-3 SH encode, a 16-line FDN per band fed at the
+predelay, lines -> SH through g_reverb,b * D_b * E, and the overlap-save
+binaural decode of the 16-channel bus -- 2(n+1)^2 = 32 convolutions per
+block regardless of the source count.  Semantics: DESIGN.md
+3.7; CPU restatement: oracle/audio.py.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+FS = 48000.0
+BLOCK = 512
+N_LINES = 16
+EDGES = (176.0, 775.0, 3408.0)
+
+
+class AudioConfig(ctypes.Structure):
+    _fields_ = [("n_sources", ctypes.c_int32), ("hist_len", ctypes.c_int32),
+                ("line_len", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+def _biquad(kind, f0, q=1.0 / np.sqrt(2.0)):
+    w0 = 2.0 * np.pi * f0 / FS
+    c, s = np.cos(w0), np.sin(w0)
+    al = s / (2.0 * q)
+    b = {"lp": [(1 - c) / 2, 1 - c, (1 - c) / 2], "hp": [(1 + c) / 2, -(1 + c), (1 + c) / 2],
+         "ap": [1 - al, -2 * c, 1 + al]}[kind]
+    a0, a1, a2 = 1 + al, -2 * c, 1 - al
+    return [b[0] / a0, b[1] / a0, b[2] / a0, a1 / a0, a2 / a0]
+
+
+def crossover_sos() -> np.ndarray:
+    """(4 bands, 5 biquads, [b0 b1 b2 a1 a2]): LR4 tree at 176/775/3408 Hz
+    with allpass compensation so the band sum is allpass."""
+    f1, f2, f3 = EDGES
+    lr = lambda k, f: [_biquad(k, f), _biquad(k, f)]  # noqa: E731
+    return np.array([lr("lp", f2) + lr("lp", f1) + [_biquad("ap", f3)],
+                     lr("lp", f2) + lr("hp", f1) + [_biquad("ap", f3)],
+                     lr("hp", f2) + lr("lp", f3) + [_biquad("ap", f1)],
+                     lr("hp", f2) + lr("hp", f3) + [_biquad("ap", f1)]], dtype=np.float32)
+
+
+def line_directions() -> np.ndarray:
+    i = np.arange(N_LINES)
+    z = 1.0 - (2.0 * i + 1.0) / N_LINES
+    r = np.sqrt(1.0 - z * z)
+    phi = i * np.pi * (3.0 - np.sqrt(5.0))
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+
+
+def _split_delay(D):
+    D = np.asarray(D, np.float64)
+    fl = np.floor(D)
+    return fl.astype(np.int32), (1.0 - (D - fl)).astype(np.float32)
+
+
+class SHRenderer:
+    """Device state + launches of ef_audio_* for S sources."""
+
+    def __init__(self, params: dict, hist_len: int = 16384, line_len: int = 4096):
+        from .sh import eval_sh_batch
+        p = params
+        S = p["dir_direct"].shape[0]
+        self.S = S
+        Y = eval_sh_batch(p["dir_direct"], 3).astype(np.float32)
+        E = eval_sh_batch(line_directions(), 3).T * np.sqrt(4.0 * np.pi / N_LINES)   # (16 sh, 16 lines)
+        m = p["fdn_delay"].astype(np.int32)
+        g_line = (10.0 ** (-3.0 * m[:, None, :].astype(np.float64) / (FS * p["rt60"][:, :, None])))
+        M = p["g_reverb"][:, :, None, None] * np.einsum("sbkj,ji->sbki", p["D"], E)
+        H = np.fft.rfft(np.concatenate([p["hrtf"], np.zeros(p["hrtf"].shape[:2] + (1024 - p["hrtf"].shape[2],))],
+                                       axis=2), axis=2).astype(np.complex64)
+        d_int, d_w = _split_delay(p["delay_direct"])
+        p_int, p_w = _split_delay(p["predelay"])
+        arrs = dict(sos=crossover_sos(), Y=Y, d_int=d_int, d_w=d_w,
+                    gain=p["gain_direct"].astype(np.float32), p_int=p_int, p_w=p_w, m=m,
+                    g=g_line.astype(np.float32), M=M.astype(np.float32),
+                    H=np.ascontiguousarray(H).view(np.float32))
+        self._host = {k: np.ascontiguousarray(v) for k, v in arrs.items()}
+        cfg = AudioConfig(S, hist_len, line_len, 0)
+        h = ctypes.c_void_p()
+        a = self._host
+        _lib.check(_lib.lib().ef_audio_create(
+            ctypes.byref(cfg), *[_lib.host_ptr(a[k]) for k in
+                                 ("sos", "Y", "d_int", "d_w", "gain", "p_int", "p_w", "m", "g", "M", "H")],
+            ctypes.byref(h)))
+        self._h = h
+        t = _lib.torch()
+        dev = _lib.device()
+        self.bus = t.zeros((16, BLOCK), dtype=t.float32, device=dev)
+        self.out = t.zeros((2, BLOCK), dtype=t.float32, device=dev)
+
+    def device_bytes(self) -> int:
+        o = np.zeros(4, np.int64)
+        _lib.check(_lib.lib().ef_audio_info(self._h, _lib.host_ptr(o)))
+        return int(o[1])
+
+    def process(self, x, want_bus: bool = True, stream=None):
+        """x: (S, 512) f32 (numpy or CUDA tensor) -> (bus (16,512), out (2,512))."""
+        t = _lib.torch()
+        is_np = not (isinstance(x, t.Tensor) and x.is_cuda)
+        xd = _lib.to_device(x, t.float32, (self.S, BLOCK))
+        _lib.check(_lib.lib().ef_audio_process(self._h, _lib.ptr(xd),
+                                               _lib.ptr(self.bus) if want_bus else None,
+                                               _lib.ptr(self.out), _lib.stream_handle(stream)))
+        if is_np:
+            return self.bus.cpu().numpy(), self.out.cpu().numpy()
+        return self.bus, self.out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.ef_audio_destroy(h)
+            self._h = None

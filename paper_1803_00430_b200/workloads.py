@@ -253,3 +253,69 @@ def c5_city_grid(nx: int = 50, ny: int = 40, nh: int = 6, nv: int = 10,
 
 
 WORKLOADS = {"c1": c1_shoebox, "c2": c2_city, "c3": c3_interior, "c5": c5_city_grid}
+
+
+def _sh3_np(d):
+    """Order-3 real SH (sh.py:94-115 formulas) for synthetic-parameter
+    generation only; the render path uses the device eval_sh."""
+    d = np.asarray(d, np.float64).reshape(-1, 3)
+    x, y, z = d[:, 0], d[:, 1], d[:, 2]
+    xx, yy, zz = x * x, y * y, z * z
+    return np.stack([
+        np.full_like(x, 0.28209479177387814), -0.4886025119029199 * y, 0.4886025119029199 * z,
+        -0.4886025119029199 * x, 1.0925484305920792 * x * y, -1.0925484305920792 * y * z,
+        0.31539156525252005 * (2.0 * zz - xx - yy), -1.0925484305920792 * x * z,
+        0.5462742152960396 * (xx - yy), -0.5900435899266435 * y * (3.0 * xx - yy),
+        2.890611442640554 * x * y * z, -0.4570457994644658 * y * (4.0 * zz - xx - yy),
+        0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy),
+        -0.4570457994644658 * x * (4.0 * zz - xx - yy), 1.445305721320277 * z * (xx - yy),
+        -0.5900435899266435 * x * (xx - 3.0 * yy)], axis=1)
+
+
+def pink_noise(n_sources: int, n_samples: int, seed: int = 4) -> np.ndarray:
+    """Seeded pink noise (Kellet's three-pole filter on white noise), f32."""
+    rng = _rng(seed, 7)
+    w = rng.standard_normal((n_sources, n_samples))
+    out = np.zeros_like(w)
+    b0 = np.zeros(n_sources)
+    b1 = np.zeros(n_sources)
+    b2 = np.zeros(n_sources)
+    for i in range(n_samples):
+        wi = w[:, i]
+        b0 = 0.99765 * b0 + wi * 0.0990460
+        b1 = 0.96300 * b1 + wi * 0.2965164
+        b2 = 0.57000 * b2 + wi * 1.0526913
+        out[:, i] = b0 + b1 + b2 + wi * 0.1848
+    return (0.1 * out).astype(np.float32)
+
+
+def c4_params(n_sources: int = 64, seed: int = 4) -> dict:
+    """C4: per-source estimated parameters (C1/C2-like ranges), FDN delays
+    ~U[20, 80] ms, and 16x2 seeded exponentially decaying 256-tap filters."""
+    rng = _rng(seed, 0)
+    S = n_sources
+    d = rng.standard_normal((S, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    dist = rng.uniform(2.0, 30.0, size=S)
+    fs = 48000.0
+    rt60 = rng.uniform(0.4, 1.5, size=(S, 4))
+    total = rng.uniform(0.005, 0.05, size=(S, 4))
+    g_reverb = np.sqrt(total / (rt60 / (6.0 * np.log(10.0))))
+    # directional loudness from a random non-negative-ish order-3 distribution
+    # on the 48-point design (sh.py:240-253 formula)
+    from .tdesigns import design_for_order
+    B = _sh3_np(design_for_order(3).directions)
+    D = np.zeros((S, 4, 16, 16))
+    for s in range(S):
+        for b in range(4):
+            avg = rng.normal(scale=0.05, size=16)
+            avg[0] = 0.28209479177387814
+            g = np.maximum(0.0, B @ avg)
+            D[s, b] = (4.0 * np.pi / len(B)) * (B.T * g) @ B
+    h_rng = _rng(seed, 1)
+    tau = 32.0
+    hrtf = (h_rng.standard_normal((16, 2, 256)) * np.exp(-np.arange(256) / tau) / 16.0)
+    return dict(dir_direct=d, delay_direct=dist / 343.0 * fs, gain_direct=(1.0 / dist)[:, None] * np.ones((1, 4)),
+                predelay=dist / 343.0 * fs + rng.uniform(0.005, 0.02, size=S) * fs,
+                fdn_delay=np.round(rng.uniform(0.020, 0.080, size=(S, 16)) * fs).astype(np.int32),
+                rt60=rt60, g_reverb=g_reverb, D=D, hrtf=hrtf, hrtf_tau=tau)

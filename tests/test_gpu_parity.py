@@ -425,3 +425,49 @@ def test_c3_dynamic_frames_and_cache():
     np.testing.assert_allclose(cache.cpu().numpy(), expect, rtol=1e-5, atol=1e-12)
     res = an.results()
     assert all(np.all(r.rt60 > 0.05) for r in res)
+
+
+# ------------------------------------------------------- C4 auralization
+def _err_db(a, ref):
+    return 10 * np.log10(np.sum((a - ref) ** 2) / max(np.sum(ref ** 2), 1e-300))
+
+
+def test_c4_render_matches_oracle():
+    """SH bus and binaural output of 8 sources over 24 blocks vs the f64
+    oracle (direct convolution): error <= -80 dB relative to signal."""
+    from oracle import audio as OA4
+    from paper_1803_00430_b200 import render
+    p = workloads.c4_params(n_sources=8)
+    x = workloads.pink_noise(8, 24 * 512)
+    r = render.SHRenderer(p)
+    ora = OA4.AudioOracle(p, p["hrtf"])
+    bus_g, out_g, bus_o, out_o = [], [], [], []
+    for k in range(24):
+        blk = x[:, k * 512:(k + 1) * 512]
+        b, o = r.process(blk)
+        bo, oo = ora.process(blk)
+        bus_g.append(b.copy()); out_g.append(o.copy()); bus_o.append(bo); out_o.append(oo)
+    bus_g, bus_o = np.concatenate(bus_g, 1), np.concatenate(bus_o, 1)
+    out_g, out_o = np.concatenate(out_g, 1), np.concatenate(out_o, 1)
+    assert np.sum(out_o ** 2) > 0 and np.abs(bus_o[:, -512:]).max() > 0
+    assert _err_db(bus_g, bus_o) <= -80.0, _err_db(bus_g, bus_o)
+    assert _err_db(out_g, out_o) <= -80.0, _err_db(out_g, out_o)
+
+
+def test_c4_crossover_and_constant_cost_properties():
+    """SPEC.md:394-396: band sum of the crossover is allpass (flat magnitude);
+    SPEC.md:497: binaural cost is 2(n+1)^2 = 32 convolutions independent of S."""
+    from oracle import audio as OA4
+    from scipy import signal
+    from paper_1803_00430_b200 import render
+    sos = render.crossover_sos().astype(np.float64)
+    w = np.linspace(20, 0.9 * 24000, 400)
+    tot = 0
+    for b in range(4):
+        s6 = np.concatenate([sos[b][:, :3], np.ones((5, 1)), sos[b][:, 3:]], axis=1)
+        _, h = signal.sosfreqz(s6, worN=w, fs=48000)
+        tot = tot + h
+    assert np.abs(20 * np.log10(np.abs(tot))).max() < 0.5
+    np.testing.assert_allclose(sos, np.array(OA4.band_sos())[:, :, [0, 1, 2, 4, 5]], rtol=1e-6, atol=1e-7)
+    p = workloads.c4_params(n_sources=2)
+    assert p["hrtf"].shape == (16, 2, 256)   # 16 SH channels x 2 ears = 32 filters
