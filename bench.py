@@ -355,12 +355,127 @@ def run_gpu(args, w, metric, unit):
         dist.destroy_process_group()
 
 
+def run_c4(args):
+    """C4: sources rendered per 512-sample block within the 10.667 ms
+    deadline (BASELINE configs[3]).  Sweeps S geometrically, then bisects
+    between the last passing and first failing count; one step = one block
+    for all S sources (crossover, taps, FDN, SH bus, binaural)."""
+    import torch
+
+    from paper_1803_00430_b200 import _lib, render, workloads
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    deadline_ms = 512 / 48000 * 1e3
+    base = workloads.c4_params(n_sources=64)
+    free, total = torch.cuda.mem_get_info()
+    per_src = 4 * 16384 * 4 + 4 * 16 * 4096 * 4 + 4 * 4 * 16 * 16 + 2048 + 512
+    s_cap = int(0.85 * free / per_src)
+
+    def params(S):
+        reps = (S + 63) // 64
+        out = {}
+        for k, v in base.items():
+            if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == 64:
+                out[k] = np.concatenate([v] * reps)[:S]
+            else:
+                out[k] = v
+        return out
+
+    def measure(S, steps):
+        r = render.SHRenderer(params(S))
+        x = torch.randn((S, 512), dtype=torch.float32, device=dev) * 0.1
+        for _ in range(args.warmup):
+            r.process(x, want_bus=False)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        n0 = _lib.launch_count()
+        for a, b in ev:
+            a.record()
+            r.process(x, want_bus=False)
+            b.record()
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        launches = _lib.launch_count() - n0
+        # e2e: pinned host input block in, binaural block out, per block
+        xh = torch.randn((S, 512), dtype=torch.float32).pin_memory()
+        oh = torch.empty((2, 512), dtype=torch.float32).pin_memory()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev2:
+            a.record()
+            x.copy_(xh, non_blocking=True)
+            r.process(x, want_bus=False)
+            oh.copy_(r.out, non_blocking=True)
+            b.record()
+        torch.cuda.synchronize()
+        e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in ev2]))
+        del r, x
+        torch.cuda.empty_cache()
+        return ms, e2e_ms, launches
+
+    sweep = []
+    S = 64
+    last_ok = None
+    first_bad = None
+    with ClockSampler(local) as clocks:
+        while S <= s_cap:
+            ms, e2e_ms, launches = measure(S, args.steps)
+            sweep.append({"sources": S, "ms_per_block": round(ms, 4), "e2e_ms_per_block": round(e2e_ms, 4)})
+            if ms <= deadline_ms:
+                last_ok = (S, ms, e2e_ms, launches)
+                S *= 2
+            else:
+                first_bad = S
+                break
+        if first_bad is None and last_ok and last_ok[0] < s_cap:
+            first_bad = s_cap + 1
+        lo = last_ok[0] if last_ok else 0
+        hi = first_bad if first_bad else lo
+        for _ in range(4):
+            if hi - lo <= max(64, lo // 32):
+                break
+            mid = (lo + hi) // 2
+            if mid > s_cap:
+                break
+            ms, e2e_ms, launches = measure(mid, args.steps)
+            sweep.append({"sources": mid, "ms_per_block": round(ms, 4), "e2e_ms_per_block": round(e2e_ms, 4)})
+            if ms <= deadline_ms:
+                lo, last_ok = mid, (mid, ms, e2e_ms, launches)
+            else:
+                hi = mid
+    S_max, ms, e2e_ms, launches = last_ok
+    # e2e: largest S whose host-in/host-out block also meets the deadline
+    e2e_ok = [p["sources"] for p in sweep if p["e2e_ms_per_block"] <= deadline_ms]
+    bytes_per_src = (8192 + 16384 + 2 * 16 * 4 * 512 * 4 + 4096 + 2048)   # DESIGN.md 5 (C4)
+    achieved = bytes_per_src * S_max / (ms * 1e-3) / 1e9
+    peak, kind = measured_peaks()
+    line = {"metric": "sources rendered per audio block within the 10.667 ms deadline",
+            "value": S_max, "unit": "sources/block", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c4_auralization (BASELINE.json configs[3])", "block": 512,
+                       "fs": 48000, "sh_order": 3, "fdn_lines_per_band": 16, "bands": 4,
+                       "hrtf": "16x2 x 256 taps, overlap-save FFT 1024",
+                       "memory_cap_sources": s_cap, "l2": "state > L2 (HBM-resident)"},
+            "e2e": {"value": max(e2e_ok) if e2e_ok else 0, "unit": "sources/block",
+                    "h2d_bytes_per_step": S_max * 512 * 4, "d2h_bytes_per_step": 2 * 512 * 4,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": kind,
+                         "kernel": "xover+render+reduce+bus", "algorithmic_bytes_per_source": bytes_per_src},
+            "sweep": sweep, "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(WORK))
+    ap.add_argument("--config", default="c2", choices=sorted(WORK) + ["c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-fraction", type=float, default=None,
                     help="fraction of each source's rays in the CPU sample (default per config)")
@@ -370,6 +485,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1803_00430_b200 import workloads
+    if args.config == "c4":
+        args.steps = min(args.steps, 20)
+        return run_c4(args)
     w = workloads.WORKLOADS[args.config]()
     if args.cpu_fraction is None:
         args.cpu_fraction = {"c1": 1.0, "c2": 1.0, "c3": 1.0 / 32, "c5": 1.0 / 1024}[args.config]
