@@ -467,6 +467,21 @@ def run_c4(args):
                          "frac": achieved / peak, "traffic": None, "peak_source": kind,
                          "kernel": "xover+render+reduce+bus", "algorithmic_bytes_per_source": bytes_per_src},
             "sweep": sweep, "clocks": clocks.summary()}
+    if not args.no_cpu_baseline:
+        from oracle import audio as OA4
+        S_cpu = 8
+        p8 = workloads.c4_params(n_sources=S_cpu)
+        xs = workloads.pink_noise(S_cpu, 512 * 6)
+        ora = OA4.AudioOracle(p8, p8["hrtf"])
+        ora.process(xs[:, :512])
+        t0 = time.perf_counter()
+        for k in range(1, 6):
+            ora.process(xs[:, k * 512:(k + 1) * 512])
+        per_block = (time.perf_counter() - t0) / 5
+        line["cpu_baseline"] = {"value": S_cpu * deadline_ms * 1e-3 / per_block, "unit": "sources/block",
+                                "cores": 1, "kind": "port",
+                                "sample": f"oracle/audio.py (f64 numpy) on {S_cpu} sources x 5 blocks, "
+                                          f"{per_block * 1e3:.1f} ms per block"}
     print(json.dumps(line), flush=True)
 
 
