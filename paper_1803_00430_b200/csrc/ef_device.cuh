@@ -240,7 +240,9 @@ __device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
 }
 
 __device__ __forceinline__ int32_t pick(const int4& c, uint32_t slot) {
-    return slot == 0 ? c.x : slot == 1 ? c.y : slot == 2 ? c.z : c.w;
+    const int32_t a = (slot & 1u) ? c.y : c.x;   // two-level select, no branches
+    const int32_t b = (slot & 1u) ? c.w : c.z;
+    return (slot & 2u) ? b : a;
 }
 
 // Leaf: exact tests of up to 8 consecutive triangles of the leaf-ordered
@@ -266,26 +268,53 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
     }
 }
 
+// Traversal stack: entries [0, kSmemStack) live in shared memory (i-major,
+// one column per thread: conflict-free and immune to L1 thrashing by node and
+// triangle traffic), deeper entries in local memory.  Entry = (node, key).
+constexpr int kSmemStack = 16;
+
+struct TravStack {
+    uint2* s;        // shared column base (nullptr: local only)
+    int stride;      // blockDim.x
+    uint2 l[kStackSize];
+    int sp;
+
+    __device__ __forceinline__ void push(int32_t node, uint32_t key) {
+        const uint2 e = make_uint2((uint32_t)node, key);
+        if (s != nullptr && sp < kSmemStack) s[sp * stride] = e;
+        else l[sp] = e;
+        ++sp;
+    }
+    __device__ __forceinline__ uint2 top() const {
+        return (s != nullptr && sp < kSmemStack) ? s[sp * stride] : l[sp];
+    }
+};
+
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
 // equal t resolves to the lowest triangle id, so the answer is independent of
-// the tree and of the traversal order.  Children are visited
-// nearest-first (packed-key sorting network); nodes [0, n_smem) are read from
-// the shared-memory copy of the top of the tree.
+// the tree and of the traversal order.  While-while form
+// (Aila & Laine 2009): each lane descends through inner nodes (nearest child
+// first, packed-key sorting network, farther hits pushed) until it holds a
+// leaf, so the expensive f64 leaf tests of a warp run together.  Nodes
+// [0, n_smem) are read from the shared-memory copy of the top of the tree.
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max, const float4* s_nodes, int n_smem,
-                                           uint32_t& n_nodes, uint32_t& n_tris) {
+                                           uint32_t& n_nodes, uint32_t& n_tris,
+                                           uint2* s_stack = nullptr) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = __double2float_ru(t_max);
-    int32_t stack_node[kStackSize];
-    uint32_t stack_key[kStackSize];
-    int sp = 0;
+    TravStack st;
+    st.s = s_stack;
+    st.stride = blockDim.x;
+    st.sp = 0;
     int32_t node = 0;
+    bool done = false;
     for (;;) {
-        if (node >= 0) {
+        while (node >= 0) {
             ++n_nodes;
             float4 nx, fx, ny, fy, nz, fz;
             int4 ch;
@@ -311,24 +340,40 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
-            if (k3 != 0xffffffffu) { stack_node[sp] = pick(ch, k3 & 3u); stack_key[sp] = k3; ++sp; }
-            if (k2 != 0xffffffffu) { stack_node[sp] = pick(ch, k2 & 3u); stack_key[sp] = k2; ++sp; }
-            if (k1 != 0xffffffffu) { stack_node[sp] = pick(ch, k1 & 3u); stack_key[sp] = k1; ++sp; }
+            if (k3 != 0xffffffffu) st.push(pick(ch, k3 & 3u), k3);
+            if (k2 != 0xffffffffu) st.push(pick(ch, k2 & 3u), k2);
+            if (k1 != 0xffffffffu) st.push(pick(ch, k1 & 3u), k1);
             if (k0 != 0xffffffffu) {
                 node = pick(ch, k0 & 3u);
                 continue;
             }
-        } else {
-            leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
+            // no child hit: pop the next node still in front of the closest
+            // hit (the key's t is rounded down, so the cull is conservative)
+            for (;;) {
+                if (st.sp == 0) {
+                    done = true;
+                    break;
+                }
+                --st.sp;
+                const uint2 e = st.top();
+                if (__uint_as_float(e.y & ~3u) <= tb) {
+                    node = (int32_t)e.x;
+                    break;
+                }
+            }
+            if (done) break;
         }
-        // pop the next node still in front of the current closest hit (the
-        // key's t is rounded down, so the cull stays conservative)
+        if (done) return h;
+        leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
         for (;;) {
-            if (sp == 0) return h;
-            --sp;
-            if (__uint_as_float(stack_key[sp] & ~3u) <= tb) break;
+            if (st.sp == 0) return h;
+            --st.sp;
+            const uint2 e = st.top();
+            if (__uint_as_float(e.y & ~3u) <= tb) {
+                node = (int32_t)e.x;
+                break;
+            }
         }
-        node = stack_node[sp];
     }
 }
 

@@ -19,8 +19,8 @@
 namespace ef {
 
 constexpr int kTraceThreads = 512;         // one fat CTA per SM (node cache in smem)
-constexpr size_t kNodeCacheBytes = 160 * 1024;
-constexpr size_t kMaxTraceSmem = 200 * 1024;
+constexpr size_t kNodeCacheBytes = 128 * 1024;   // + 64 KB of traversal stacks
+constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -108,9 +108,10 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
     unsigned int* s_stats = reinterpret_cast<unsigned int*>(s_sumt + P.n_src);
     double* s_tri = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(s_stats + P.n_src * EF_ST_COUNT) + 15) & ~uintptr_t(15));
-    // node cache after the stats, 16-byte aligned
-    float4* s_nodes = reinterpret_cast<float4*>(
+    // traversal stacks (kSmemStack entries per thread), then the node cache
+    uint2* s_stack = reinterpret_cast<uint2*>(
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
+    float4* s_nodes = reinterpret_cast<float4*>(s_stack + (BRUTE ? 0 : kSmemStack * kTraceThreads));
     if (!BRUTE) {
         const float4* g = reinterpret_cast<const float4*>(P.nodes);
         for (int i = threadIdx.x; i < 8 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
@@ -182,7 +183,8 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
         }
         else
             h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
-                            P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS]);
+                            P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
+                            s_stack + threadIdx.x);
         const bool hit = h.id != INT32_MAX;
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
@@ -299,7 +301,8 @@ static int sm_count() {
 template <int NBMAX, int ORDER, bool BRUTE>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
-                  (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode));
+                  (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode) +
+                                   (size_t)kSmemStack * kTraceThreads * sizeof(uint2));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
