@@ -271,23 +271,22 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
 // Traversal stack: entries [0, kSmemStack) live in shared memory (i-major,
 // one column per thread: conflict-free and immune to L1 thrashing by node and
 // triangle traffic), deeper entries in local memory.  Entry = (node, key).
-constexpr int kSmemStack = 16;
+constexpr int kSmemStack = 16;   // max shared entries per thread (runtime depth <= this)
 
 struct TravStack {
     uint2* s;        // shared column base (nullptr: local only)
     int stride;      // blockDim.x
+    int depth;       // shared entries per thread
     uint2 l[kStackSize];
     int sp;
 
     __device__ __forceinline__ void push(int32_t node, uint32_t key) {
         const uint2 e = make_uint2((uint32_t)node, key);
-        if (s != nullptr && sp < kSmemStack) s[sp * stride] = e;
+        if (sp < depth) s[sp * stride] = e;
         else l[sp] = e;
         ++sp;
     }
-    __device__ __forceinline__ uint2 top() const {
-        return (s != nullptr && sp < kSmemStack) ? s[sp * stride] : l[sp];
-    }
+    __device__ __forceinline__ uint2 top() const { return sp < depth ? s[sp * stride] : l[sp]; }
 };
 
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
@@ -302,7 +301,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max, const float4* s_nodes, int n_smem,
                                            uint32_t& n_nodes, uint32_t& n_tris,
-                                           uint2* s_stack = nullptr) {
+                                           uint2* s_stack = nullptr, int s_depth = 0) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
@@ -310,6 +309,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     TravStack st;
     st.s = s_stack;
     st.stride = blockDim.x;
+    st.depth = s_stack ? s_depth : 0;
     st.sp = 0;
     int32_t node = 0;
     bool done = false;

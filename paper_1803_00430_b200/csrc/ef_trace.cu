@@ -18,7 +18,14 @@
 
 namespace ef {
 
-constexpr int kTraceThreads = 512;         // one fat CTA per SM (node cache in smem)
+// One fat CTA per SM (node cache in shared memory).  Scenes whose nodes +
+// triangles exceed kBigSceneBytes (DRAM-latency-bound traversal, e.g. C5) get
+// 768 threads (80 registers, more warps to hide latency); smaller ones 512.
+constexpr int kSmallThreads = 512;
+constexpr int kBigThreads = 768;
+constexpr int64_t kBigSceneBytes = 32ll << 20;
+template <int THREADS>
+constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
 constexpr size_t kNodeCacheBytes = 128 * 1024;   // + 64 KB of traversal stacks
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
@@ -98,8 +105,8 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats
     ls.sum_t = 0.0;
 }
 
-template <int NBMAX, int ORDER, bool BRUTE>
-__global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TraceParams P) {
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
     extern __shared__ __align__(16) unsigned char smem[];
     // per-block counters: f64 path-length sums, then u32 counters (a block's
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
     // traversal stacks (kSmemStack entries per thread), then the node cache
     uint2* s_stack = reinterpret_cast<uint2*>(
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
-    float4* s_nodes = reinterpret_cast<float4*>(s_stack + (BRUTE ? 0 : kSmemStack * kTraceThreads));
+    float4* s_nodes = reinterpret_cast<float4*>(s_stack + (BRUTE ? 0 : smem_stack_depth<THREADS>() * THREADS));
     if (!BRUTE) {
         const float4* g = reinterpret_cast<const float4*>(P.nodes);
         for (int i = threadIdx.x; i < 8 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(kTraceThreads, 1) trace_kernel(const TracePara
         else
             h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
                             P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
-                            s_stack + threadIdx.x);
+                            s_stack + threadIdx.x, smem_stack_depth<THREADS>());
         const bool hit = h.id != INT32_MAX;
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
@@ -298,12 +305,12 @@ static int sm_count() {
     return n;
 }
 
-template <int NBMAX, int ORDER, bool BRUTE>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
                   (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode) +
-                                   (size_t)kSmemStack * kTraceThreads * sizeof(uint2));
-    auto kern = trace_kernel<NBMAX, ORDER, BRUTE>;
+                                   (size_t)smem_stack_depth<THREADS>() * THREADS * sizeof(uint2));
+    auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,22 +322,29 @@ static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
     // persistent grid: one 512-thread CTA per SM (__launch_bounds__(512, 1)
     // and ~100 registers leave room for exactly one), no more warps than paths
     long long want = (long long)sm_count();
-    long long need = ((long long)P.total + kTraceThreads - 1) / kTraceThreads;
+    long long need = ((long long)P.total + THREADS - 1) / THREADS;
     int grid = (int)std::max(1LL, std::min(want, need));
-    kern<<<grid, kTraceThreads, smem, st>>>(P);
+    kern<<<grid, THREADS, smem, st>>>(P);
     count_launch();
     return cudaGetLastError();
 }
 
-template <int NBMAX, bool BRUTE>
+template <int NBMAX, bool BRUTE, int THREADS>
 static cudaError_t dispatch_order(int order, const TraceParams& P, cudaStream_t st) {
     switch (order) {
-        case 0: return launch_trace<NBMAX, 0, BRUTE>(P, st);
-        case 1: return launch_trace<NBMAX, 1, BRUTE>(P, st);
-        case 2: return launch_trace<NBMAX, 2, BRUTE>(P, st);
-        case 3: return launch_trace<NBMAX, 3, BRUTE>(P, st);
-        default: return launch_trace<NBMAX, 4, BRUTE>(P, st);
+        case 0: return launch_trace<NBMAX, 0, BRUTE, THREADS>(P, st);
+        case 1: return launch_trace<NBMAX, 1, BRUTE, THREADS>(P, st);
+        case 2: return launch_trace<NBMAX, 2, BRUTE, THREADS>(P, st);
+        case 3: return launch_trace<NBMAX, 3, BRUTE, THREADS>(P, st);
+        default: return launch_trace<NBMAX, 4, BRUTE, THREADS>(P, st);
     }
+}
+
+template <int NBMAX>
+static cudaError_t dispatch(bool brute, bool big, int order, const TraceParams& P, cudaStream_t st) {
+    if (brute) return dispatch_order<NBMAX, true, kSmallThreads>(order, P, st);
+    if (big) return dispatch_order<NBMAX, false, kBigThreads>(order, P, st);
+    return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -588,10 +602,12 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
         P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, kNodeCacheBytes / sizeof(GpuNode));
+        const bool big = (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
+                             s->n_tri * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
         if (s->n_bands <= 4)
-            e = brute ? dispatch_order<4, true>(cfg->order, P, st) : dispatch_order<4, false>(cfg->order, P, st);
+            e = dispatch<4>(brute, big, cfg->order, P, st);
         else
-            e = brute ? dispatch_order<8, true>(cfg->order, P, st) : dispatch_order<8, false>(cfg->order, P, st);
+            e = dispatch<8>(brute, big, cfg->order, P, st);
         if (e != cudaSuccess) break;
     }
     cudaError_t e2 = cudaFreeAsync(counter, st);
