@@ -371,7 +371,7 @@ def run_c4(args):
     deadline_ms = 512 / 48000 * 1e3
     base = workloads.c4_params(n_sources=64)
     free, total = torch.cuda.mem_get_info()
-    per_src = 4 * 16384 * 4 + 4 * 16 * 4096 * 4 + 4 * 4 * 16 * 16 + 2048 + 512
+    per_src = 4 * 8192 * 4 + 4 * 16 * 4096 * 4 + 4 * 4 * 16 * 16 + 2048 + 512   # C4 delays fit an 8192 ring
     s_cap = int(0.85 * free / per_src)
 
     def params(S):

@@ -128,7 +128,7 @@ __device__ __forceinline__ float tap(const float* __restrict__ row, long long t,
     return __fmaf_rn(w, b - a, a);
 }
 
-__global__ void __launch_bounds__(kBlock, 1) render_kernel(AudioState A) {
+__global__ void __launch_bounds__(kBlock, 2) render_kernel(AudioState A) {
     __shared__ float s_M[kBands * kSh * kLines];
     __shared__ float s_Y[kSh];
     __shared__ float s_g[kBands * kLines];
@@ -167,43 +167,38 @@ __global__ void __launch_bounds__(kBlock, 1) render_kernel(AudioState A) {
         }
 #pragma unroll
         for (int k = 0; k < kSh; ++k) bus[k] = __fmaf_rn(s_Y[k], mono, bus[k]);
-        // FDN: read every delayed line sample first (m_i > block, so all
-        // come from earlier blocks), then write this block's line inputs
+        // FDN, one band at a time: read every delayed line sample first
+        // (m_i > block, so all come from earlier blocks), barrier (a write
+        // slot of this block can alias another thread's read slot), then
+        // write this block's line inputs and accumulate the SH output
         float* ls = A.lines + (size_t)s * kBands * kLines * A.line_len;
-        float y[kBands][kLines];
-#pragma unroll
-        for (int b = 0; b < kBands; ++b)
+#pragma unroll 1
+        for (int b = 0; b < kBands; ++b) {
+            float y[kLines];
 #pragma unroll
             for (int i = 0; i < kLines; ++i)
-                y[b][i] = ls[((size_t)b * kLines + i) * A.line_len + ((t - s_m[i]) & lmask)];
-        __syncthreads();
-#pragma unroll
-        for (int b = 0; b < kBands; ++b) {
-            float gy[kLines];
+                y[i] = ls[((size_t)b * kLines + i) * A.line_len + ((t - s_m[i]) & lmask)];
+            __syncthreads();
             float sum = 0.f;
 #pragma unroll
             for (int i = 0; i < kLines; ++i) {
-                gy[i] = s_g[b * kLines + i] * y[b][i];
-                sum += gy[i];
+                sum = __fmaf_rn(s_g[b * kLines + i], y[i], sum);
             }
             const float in = 0.25f * send[b] - (2.0f / kLines) * sum;   // Householder feedback
 #pragma unroll
             for (int i = 0; i < kLines; ++i)
-                ls[((size_t)b * kLines + i) * A.line_len + (t & lmask)] = in + gy[i];
-        }
-        // line outputs -> SH bus through g_reverb,b * D_b * E
+                ls[((size_t)b * kLines + i) * A.line_len + (t & lmask)] = __fmaf_rn(s_g[b * kLines + i], y[i], in);
+            // line outputs -> SH bus through g_reverb,b * D_b * E
 #pragma unroll
-        for (int k = 0; k < kSh; ++k) {
-            float acc = bus[k];
+            for (int k = 0; k < kSh; ++k) {
+                float acc = bus[k];
 #pragma unroll
-            for (int b = 0; b < kBands; ++b)
-#pragma unroll
-                for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(s_M[(b * kSh + k) * kLines + i], y[b][i], acc);
-            bus[k] = acc;
+                for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(s_M[(b * kSh + k) * kLines + i], y[i], acc);
+                bus[k] = acc;
+            }
         }
         __syncthreads();
     }
-#pragma unroll
     for (int k = 0; k < kSh; ++k) A.partial[((size_t)blockIdx.x * kSh + k) * kBlock + n] = bus[k];
 }
 
@@ -338,7 +333,7 @@ extern "C" int ef_audio_create(const ef_audio_config* cfg, const float* sos, con
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    A.grid = std::min(S, 2 * sms);
+    A.grid = std::min(S, 4 * sms);   // two 512-thread CTAs per SM, two waves
     cudaError_t e = cudaSuccess;
 #define UP(f, src, n) if (e == cudaSuccess) e = up(&A.f, src, (size_t)(n), A.bytes);
     UP(sos, sos, kBands * kBiquads * 5);

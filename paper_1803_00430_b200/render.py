@@ -65,7 +65,7 @@ def _split_delay(D):
 class SHRenderer:
     """Device state + launches of ef_audio_* for S sources."""
 
-    def __init__(self, params: dict, hist_len: int = 16384, line_len: int = 4096):
+    def __init__(self, params: dict, hist_len: int | None = None, line_len: int = 4096):
         from .sh import eval_sh_batch
         p = params
         S = p["dir_direct"].shape[0]
@@ -79,6 +79,10 @@ class SHRenderer:
                                        axis=2), axis=2).astype(np.complex64)
         d_int, d_w = _split_delay(p["delay_direct"])
         p_int, p_w = _split_delay(p["predelay"])
+        if hist_len is None:
+            # smallest power-of-two band history holding the longest tap + a block
+            need = int(max(d_int.max(), p_int.max())) + BLOCK + 2
+            hist_len = 1 << max(need - 1, 1).bit_length()
         arrs = dict(sos=crossover_sos(), Y=Y, d_int=d_int, d_w=d_w,
                     gain=p["gain_direct"].astype(np.float32), p_int=p_int, p_w=p_w, m=m,
                     g=g_line.astype(np.float32), M=M.astype(np.float32),
