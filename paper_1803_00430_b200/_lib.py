@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libechoforge_b200.so")
+LIB_PATH = os.environ.get("EF_LIB_PATH", os.path.join(HERE, "libechoforge_b200.so"))
 
 EF_OK, EF_EINVAL, EF_ECUDA, EF_ENOMEM, EF_EUNSUPPORTED = 0, -1, -2, -3, -4
 ST_NAMES = ("paths", "segments", "reflections", "arrivals", "direct", "dropped", "escaped",

@@ -32,24 +32,27 @@ def sources():
                   if f.endswith((".cu", ".cpp")))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, profile_phases: bool = False) -> str:
     srcs = sources()
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "echoforge_b200.h"))
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+    lib = LIB.replace(".so", "_prof.so") if profile_phases else LIB
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in deps):
-            return LIB
+            return lib
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off",
-           "-shared", "-o", LIB + ".tmp", *srcs, "-lcudart"]
+           "-shared", "-o", lib + ".tmp", *srcs, "-lcudart"]
+    if profile_phases:
+        cmd.insert(1, "-DEF_PROFILE_PHASES")
     if verbose:
         cmd.insert(-1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force=True))
+    print(build(verbose="-v" in sys.argv, force=True, profile_phases="--profile-phases" in sys.argv))

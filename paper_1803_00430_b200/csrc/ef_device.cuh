@@ -9,6 +9,17 @@
 
 namespace ef {
 
+#ifdef EF_PROFILE_PHASES
+// debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
+// 2 pops after leaves, 3 shading, 4 segments)
+extern __device__ unsigned long long g_phase[8];
+#define EF_PHASE_T0(v) const long long v = clock64()
+#define EF_PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(clock64() - (v)))
+#else
+#define EF_PHASE_T0(v)
+#define EF_PHASE_ADD(i, v)
+#endif
+
 // ---------------------------------------------------------------- RNG ----
 // Philox4x32-10 (Salmon et al. 2011); key = (seed, source key),
 // counter = (ray, bounce, draw, frame).  DESIGN.md 3.1.
@@ -315,6 +326,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     bool done = false;
     for (;;) {
         while (node >= 0) {
+            EF_PHASE_T0(tv);
             ++n_nodes;
             float4 nx, fx, ny, fy, nz, fz;
             int4 ch;
@@ -345,6 +357,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
             if (k1 != 0xffffffffu) st.push(pick(ch, k1 & 3u), k1);
             if (k0 != 0xffffffffu) {
                 node = pick(ch, k0 & 3u);
+                EF_PHASE_ADD(0, tv);
                 continue;
             }
             // no child hit: pop the next node still in front of the closest
@@ -361,10 +374,14 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                     break;
                 }
             }
+            EF_PHASE_ADD(0, tv);
             if (done) break;
         }
         if (done) return h;
+        EF_PHASE_T0(tl);
         leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
+        EF_PHASE_ADD(1, tl);
+        EF_PHASE_T0(tp);
         for (;;) {
             if (st.sp == 0) return h;
             --st.sp;
@@ -374,6 +391,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                 break;
             }
         }
+        EF_PHASE_ADD(2, tp);
     }
 }
 

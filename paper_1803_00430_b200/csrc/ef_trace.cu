@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                             P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
                             s_stack + threadIdx.x, smem_stack_depth<THREADS>());
         const bool hit = h.id != INT32_MAX;
+        EF_PHASE_T0(tsh);
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
         // ---- listener sphere receiver + SH histogram commit
@@ -272,6 +273,10 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             }
             if (nrefl >= P.max_bounces) active = false;
         }
+        EF_PHASE_ADD(3, tsh);
+#ifdef EF_PROFILE_PHASES
+        atomicAdd(&g_phase[4], 1ull);
+#endif
         if (!active && P.path_nseg) P.path_nseg[path] = nseg;
         if (!active && P.timing) {
             const unsigned long long t_end = globaltimer();
@@ -650,3 +655,14 @@ extern "C" int ef_loudness_batch(const double* avg, int64_t n, int32_t order, co
     count_launch();
     return check_cuda(cudaGetLastError(), "loudness_kernel");
 }
+
+#ifdef EF_PROFILE_PHASES
+extern "C" int ef_debug_phases(unsigned long long* out8, int reset) {
+    cudaMemcpyFromSymbol(out8, g_phase, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_phase, z, sizeof z);
+    }
+    return EF_OK;
+}
+#endif

@@ -143,3 +143,32 @@ def knobs(name="c2"):
 
 if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "knobs":
     knobs(sys.argv[1])
+
+
+def phases(name="c2", src=6, ray=27707):
+    """Cycle breakdown of one path (needs EF_LIB_PATH=..._prof.so)."""
+    import ctypes
+    from paper_1803_00430_b200 import _lib
+    L = _lib.lib()
+    L.ef_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    w = workloads.WORKLOADS[name]()
+    sc = scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = propagation.FrameTracer(sc, 1, cfg, record=2)
+    tr.set_sources(w.sources[src:src + 1], [src])
+    out = np.zeros(8, np.uint64)
+    for rep in range(3):
+        L.ef_debug_phases(out.ctypes.data, 1)
+        tr.trace(w.listener, ray_ids=[ray])
+        torch.cuda.synchronize()
+        L.ef_debug_phases(out.ctypes.data, 1)
+    segs = int(out[4])
+    names = ["inner visits", "leaf tests", "pops after leaf", "shading"]
+    print(f"[{name}] path src {src} ray {ray}: {segs} segments; cycles per segment:")
+    for i, n in enumerate(names):
+        print(f"   {n:16s} {int(out[i]) / max(segs, 1):9.0f}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "phases":
+    phases(sys.argv[1])
