@@ -326,6 +326,9 @@ def run_gpu(args, w, metric, unit):
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()   # every rank tears NCCL down before exit
     if rank != 0:
         return
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
@@ -351,8 +354,6 @@ def run_gpu(args, w, metric, unit):
                                           f"{len(w.sources)} sources ({segs_c} segments, {dt:.1f} s, "
                                           f"{cores} threads)"}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 def run_c4(args):
