@@ -159,8 +159,26 @@ typedef struct {
     float e0;               /* initial energy per band of every path       */
     int32_t record_ids;     /* nonzero: write per-segment hit ids          */
     int32_t clear_outputs;  /* nonzero: zero H, Dir, stats, sum_t first    */
-    int32_t reserved;
+    int32_t diffuse_rain;   /* nonzero: next-event connection from every
+                               diffuse bounce; segments
+                               leaving a diffuse bounce then skip the
+                               sphere test                  */
+    int32_t er_max_order;   /* arrivals of order 1..er_max_order (<= 2) go
+                               to the early-reflection list, not to H       */
+    int64_t er_capacity;    /* entries available at er_entries             */
+    void* er_entries;       /* DEVICE ef_er_entry[er_capacity] or NULL      */
+    uint32_t* er_count;     /* DEVICE counter, ACCUMULATED (caller zeroes)  */
 } ef_trace_config;
+
+/* One early-reflection arrival (PathList source data). */
+typedef struct {
+    int32_t src, order;     /* source index in the launch, reflections     */
+    int32_t tri0, tri1;     /* first two reflecting triangles (-1: none)   */
+    double dist;            /* path length to the listener, m              */
+    float dir[3];           /* arrival direction (towards the source side) */
+    float pad;
+    float energy[8];        /* per-band energy (intensity units of H)      */
+} ef_er_entry;
 
 /* DEVICE arrays:
  *   src_pos  (n_sources,3) f64      src_key (n_sources,) u32 Philox key word 1

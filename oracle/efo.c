@@ -171,6 +171,7 @@ typedef struct {
     /* reflection factors per material: diffuse / specular, f32 */
     float* fd;
     float* fs;
+    float* fr;     /* (1 - a) * s: diffusely reflected fraction (diffuse rain) */
     double* pdiff;
     /* reference BVH */
     int64_t n_nodes, cap_nodes;
@@ -340,6 +341,7 @@ static void material_tables(efo_scene* s, const double* absorption, const double
     int nb = s->n_bands;
     s->fd = calloc((size_t)s->n_mat * nb, sizeof(float));
     s->fs = calloc((size_t)s->n_mat * nb, sizeof(float));
+    s->fr = calloc((size_t)s->n_mat * nb, sizeof(float));
     s->pdiff = calloc((size_t)s->n_mat, sizeof(double));
     for (int m = 0; m < s->n_mat; ++m) {
         double p = 0.0;
@@ -351,6 +353,7 @@ static void material_tables(efo_scene* s, const double* absorption, const double
             double sb = scattering[m * nb + b];
             s->fd[m * nb + b] = p > 0.0 ? f32_of(keep * (sb / p)) : 0.0f;
             s->fs[m * nb + b] = p < 1.0 ? f32_of(keep * ((1.0 - sb) / (1.0 - p))) : 0.0f;
+            s->fr[m * nb + b] = f32_of(keep * sb);
         }
     }
 }
@@ -392,7 +395,7 @@ efo_scene* efo_scene_create(const double* v0, const double* e1, const double* e2
 
 void efo_scene_destroy(efo_scene* s) {
     if (!s) return;
-    free(s->fd); free(s->fs); free(s->pdiff);
+    free(s->fd); free(s->fs); free(s->fr); free(s->pdiff);
     free(s->node_min); free(s->node_max); free(s->node_left); free(s->node_start); free(s->node_count);
     free(s->tri_order); free(s->tri_min); free(s->tri_max); free(s->cen);
     free(s);
@@ -579,6 +582,9 @@ void efo_eval_sh_batch(const double* dirs, int64_t n, int order, double* out) {
 /* ------------------------------------------------------------------ */
 /* Bounce loop (pinned in DESIGN.md 3)       */
 /* ------------------------------------------------------------------ */
+enum { ST_PATHS = 0, ST_SEGMENTS, ST_REFLECTIONS, ST_ARRIVALS, ST_DIRECT, ST_DROPPED, ST_ESCAPED,
+       ST_NODES, ST_TRIS, ST_NEARTIE_PATHS, ST_COUNT };
+
 typedef struct {
     int32_t n_bands, order, n_bins, max_bounces;
     double bin_len;        /* meters per IR bin = c * bin_s */
@@ -588,10 +594,60 @@ typedef struct {
     int32_t vmode;         /* 1: OpenBLAS order for v on BVH leaves (pin only) */
     int32_t mode;          /* 0 reference dispatch, 1 brute, 2 bvh */
     float e0;              /* initial per-band energy of every path */
+    int32_t rain;          /* diffuse rain */
+    int32_t er_max_order;  /* arrivals of order 1..er_max_order -> ER list */
 } efo_trace_cfg;
 
-enum { ST_PATHS = 0, ST_SEGMENTS, ST_REFLECTIONS, ST_ARRIVALS, ST_DIRECT, ST_DROPPED, ST_ESCAPED,
-       ST_NODES, ST_TRIS, ST_NEARTIE_PATHS, ST_COUNT };
+typedef struct {
+    int32_t src, order, tri0, tri1;
+    double dist;
+    float dir[3];
+    float pad;
+    float energy[8];
+} efo_er_entry;
+
+typedef struct {
+    double* H;
+    double* Dir;
+    uint64_t* stats;
+    efo_er_entry* er;
+    int64_t er_cap;
+    int64_t* er_count;
+} efo_sink;
+
+/* one arrival: order 0 -> Dir, 1..er_max_order -> ER list, else H bin */
+static void commit(const efo_trace_cfg* cfg, efo_sink* k, uint32_t src_key, int order, int tri0,
+                   int tri1, double dist, double ux, double uy, double uz, const float* c) {
+    const int nb = cfg->n_bands;
+    const int nk = (cfg->order + 1) * (cfg->order + 1);
+    k->stats[ST_ARRIVALS]++;
+    double* dst = NULL;
+    if (order == 0) {
+        k->stats[ST_DIRECT]++;
+        dst = k->Dir;
+    } else if (order <= cfg->er_max_order) {
+        if (*k->er_count < k->er_cap) {
+            efo_er_entry* e = &k->er[*k->er_count];
+            e->src = (int32_t)src_key; e->order = order; e->tri0 = tri0; e->tri1 = tri1;
+            e->dist = dist;
+            e->dir[0] = (float)ux; e->dir[1] = (float)uy; e->dir[2] = (float)uz; e->pad = 0.f;
+            for (int b = 0; b < 8; ++b) e->energy[b] = b < nb ? c[b] : 0.f;
+        }
+        (*k->er_count)++;
+        return;
+    } else {
+        double q = dist / cfg->bin_len;
+        if (q < (double)cfg->n_bins) dst = &k->H[(int64_t)q * nb * nk];
+        else k->stats[ST_DROPPED]++;
+    }
+    if (dst) {
+        double dir[3] = {ux, uy, uz}, Y[EFO_MAX_NK];
+        efo_eval_sh(dir, cfg->order, Y);
+        for (int b = 0; b < nb; ++b)
+            for (int kk = 0; kk < nk; ++kk) dst[b * nk + kk] += (double)(c[b] * (float)Y[kk]);
+    }
+}
+
 
 /* Trace rays ray_ids[0..n) (or ray0 + i when ray_ids is NULL) of one source.
  * H: (n_bins, n_bands, nk) f64 accumulator, Dir: (n_bands, nk) f64.
@@ -602,9 +658,11 @@ enum { ST_PATHS = 0, ST_SEGMENTS, ST_REFLECTIONS, ST_ARRIVALS, ST_DIRECT, ST_DRO
 void efo_trace(const efo_scene* s, const efo_trace_cfg* cfg, uint32_t src_key,
                const double* src_pos, const uint32_t* ray_ids, uint32_t ray0, int64_t n,
                double* H, double* Dir, uint64_t* stats, double* sum_t,
-               int32_t* nseg_out, int32_t* ids_out, int32_t* first_tie_out) {
+               int32_t* nseg_out, int32_t* ids_out, int32_t* first_tie_out,
+               efo_er_entry* er, int64_t er_cap, int64_t* er_count) {
+    int64_t er_dummy = 0;
+    efo_sink sink = {H, Dir, stats, er, er_cap, er_count ? er_count : &er_dummy};
     const int nb = cfg->n_bands;
-    const int nk = (cfg->order + 1) * (cfg->order + 1);
     int64_t* stack = malloc(sizeof(int64_t) * 4096);
     int brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= EFO_BRUTE_MAX);
     const double r2 = cfg->radius * cfg->radius;
@@ -617,6 +675,7 @@ void efo_trace(const efo_scene* s, const efo_trace_cfg* cfg, uint32_t src_key,
         for (int b = 0; b < nb; ++b) E[b] = cfg->e0;
         double plen = 0.0;
         int nrefl = 0, nseg = 0, first_tie = -1;
+        int tri0 = -1, tri1 = -1, last_diffuse = 0;
         stats[ST_PATHS]++;
         for (;;) {
             hit_info h;
@@ -632,35 +691,17 @@ void efo_trace(const efo_scene* s, const efo_trace_cfg* cfg, uint32_t src_key,
                 if (m < 1e-6 || h.tie) first_tie = nseg;
             }
             if (ids_out) ids_out[i * cfg->max_bounces + nseg] = (int32_t)h.tri;
-            /* listener sphere receiver */
-            double Lo[3] = {cfg->listener[0] - o[0], cfg->listener[1] - o[1], cfg->listener[2] - o[2]};
-            double tc = dot3(Lo, d);
-            double tlim = hit ? h.t : INFINITY;
-            if (tc > 0.0 && tc < tlim) {
-                double dist2 = dot3(Lo, Lo);
-                double perp2 = dist2 - tc * tc;
-                if (perp2 <= r2) {
-                    double nd[3] = {-d[0], -d[1], -d[2]};
-                    double Y[EFO_MAX_NK];
-                    efo_eval_sh(nd, cfg->order, Y);
-                    stats[ST_ARRIVALS]++;
-                    if (nrefl == 0) {
-                        stats[ST_DIRECT]++;
-                        for (int b = 0; b < nb; ++b)
-                            for (int k = 0; k < nk; ++k)
-                                Dir[b * nk + k] += (double)(E[b] * (float)Y[k]);
-                    } else {
-                        double q = (plen + tc) / cfg->bin_len;
-                        if (q < (double)cfg->n_bins) {
-                            int64_t bin = (int64_t)q;
-                            double* row = &H[bin * nb * nk];
-                            for (int b = 0; b < nb; ++b)
-                                for (int k = 0; k < nk; ++k)
-                                    row[b * nk + k] += (double)(E[b] * (float)Y[k]);
-                        } else {
-                            stats[ST_DROPPED]++;
-                        }
-                    }
+            /* listener sphere receiver (skipped after a diffuse bounce when
+             * diffuse rain is the listener connection) */
+            if (!(cfg->rain && last_diffuse)) {
+                double Lo[3] = {cfg->listener[0] - o[0], cfg->listener[1] - o[1], cfg->listener[2] - o[2]};
+                double tc = dot3(Lo, d);
+                double tlim = hit ? h.t : INFINITY;
+                if (tc > 0.0 && tc < tlim) {
+                    double dist2 = dot3(Lo, Lo);
+                    double perp2 = dist2 - tc * tc;
+                    if (perp2 <= r2) commit(cfg, &sink, src_key, nrefl, tri0, tri1, plen + tc,
+                                            -d[0], -d[1], -d[2], E);
                 }
             }
             nseg++;
@@ -674,15 +715,44 @@ void efo_trace(const efo_scene* s, const efo_trace_cfg* cfg, uint32_t src_key,
             o[1] = o[1] + t * d[1];
             o[2] = o[2] + t * d[2];
             nrefl++;
+            if (nrefl == 1) tri0 = (int)h.tri;
+            if (nrefl == 2) tri1 = (int)h.tri;
             stats[ST_REFLECTIONS]++;
             int64_t m = s->mat[h.tri];
             const double* nrm = &s->normals[3 * h.tri];
             double u1, u2;
             draw2(ray, (uint32_t)nrefl, 0u, cfg->frame, cfg->seed, src_key, &u1, &u2);
             int diffuse = u1 < s->pdiff[m];
+            double nd = dot3(nrm, d);
+            if (cfg->rain && diffuse) {
+                /* diffuse rain: c_b = E_b (1-a_b) s_b cos r^2 / d^2 if visible */
+                double sg = nd > 0.0 ? -1.0 : 1.0;
+                double L[3] = {cfg->listener[0] - o[0], cfg->listener[1] - o[1], cfg->listener[2] - o[2]};
+                double d2 = dot3(L, L);
+                double dd = sqrt(d2);
+                double sn[3] = {sg * nrm[0], sg * nrm[1], sg * nrm[2]};
+                double cosv = dot3(sn, L) / dd;
+                if (cosv > 0.0 && dd > EFO_RAY_EPS) {
+                    double e[3] = {L[0] / dd, L[1] / dd, L[2] / dd};
+                    double limit = dd - EFO_RAY_EPS;
+                    hit_info sh;
+                    if (brute) {
+                        brute_intersect(s, o, e, EFO_RAY_EPS, &sh);
+                        if (sh.tri >= 0 && !(sh.t <= limit)) sh.tri = -1;
+                    } else {
+                        bvh_intersect(s, o, e, EFO_RAY_EPS, limit, cfg->vmode, &sh, stack);
+                    }
+                    if (sh.tri < 0) {
+                        float gf = (float)(cosv * r2 / d2);
+                        float c[EFO_MAX_BANDS];
+                        for (int b = 0; b < nb; ++b) c[b] = E[b] * s->fr[m * nb + b] * gf;
+                        commit(cfg, &sink, src_key, nrefl, tri0, tri1, plen + dd, -e[0], -e[1], -e[2], c);
+                    }
+                }
+            }
+            last_diffuse = diffuse;
             const float* f = diffuse ? &s->fd[m * nb] : &s->fs[m * nb];
             for (int b = 0; b < nb; ++b) E[b] = E[b] * f[b];
-            double nd = dot3(nrm, d);
             if (diffuse) {
                 double nn[3] = {nrm[0], nrm[1], nrm[2]};
                 if (nd > 0.0) { nn[0] = -nn[0]; nn[1] = -nn[1]; nn[2] = -nn[2]; }

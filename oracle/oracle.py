@@ -61,7 +61,7 @@ def lib():
         L.efo_philox.argtypes = [vp, vp, vp]
         L.efo_sample_sphere.argtypes = [ctypes.c_uint32] * 4 + [vp]
         L.efo_trace.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint32,
-                                ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp]
+                                ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp]
         _lib = L
     return _lib
 
@@ -80,7 +80,18 @@ class _TraceCfg(ctypes.Structure):
                 ("bin_len", ctypes.c_double), ("listener", ctypes.c_double * 3),
                 ("radius", ctypes.c_double), ("seed", ctypes.c_uint32),
                 ("frame", ctypes.c_uint32), ("vmode", ctypes.c_int32),
-                ("mode", ctypes.c_int32), ("e0", ctypes.c_float)]
+                ("mode", ctypes.c_int32), ("e0", ctypes.c_float),
+                ("rain", ctypes.c_int32), ("er_max_order", ctypes.c_int32)]
+
+
+class ErEntry(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_int32), ("order", ctypes.c_int32), ("tri0", ctypes.c_int32),
+                ("tri1", ctypes.c_int32), ("dist", ctypes.c_double), ("dir", ctypes.c_float * 3),
+                ("pad", ctypes.c_float), ("energy", ctypes.c_float * 8)]
+
+
+ER_DTYPE = np.dtype([("src", "<i4"), ("order", "<i4"), ("tri0", "<i4"), ("tri1", "<i4"),
+                     ("dist", "<f8"), ("dir", "<f4", 3), ("pad", "<f4"), ("energy", "<f4", 8)])
 
 
 def philox(ctr, key):
@@ -176,11 +187,12 @@ class OracleTrace:
     nseg: np.ndarray | None
     ids: np.ndarray | None
     first_tie: np.ndarray | None
+    er: np.ndarray | None = None
 
 
 def trace(scene: OracleScene, *, src_key, src_pos, listener, radius, seed, frame=0,
           order, n_bins, bin_len, max_bounces, e0, rays=None, ray0=0, n_rays=None,
-          record=False, mode=0, blas_v=False):
+          record=False, mode=0, blas_v=False, rain=False, er_max_order=0, er_capacity=0):
     """Pinned bounce loop for one source."""
     cfg = _TraceCfg()
     cfg.n_bands = scene.n_bands
@@ -195,6 +207,8 @@ def trace(scene: OracleScene, *, src_key, src_pos, listener, radius, seed, frame
     cfg.vmode = int(blas_v)
     cfg.mode = mode
     cfg.e0 = float(np.float32(e0))
+    cfg.rain = int(rain)
+    cfg.er_max_order = int(er_max_order)
     if rays is not None:
         rays = _c(rays, np.uint32)
         n = len(rays)
@@ -209,7 +223,10 @@ def trace(scene: OracleScene, *, src_key, src_pos, listener, radius, seed, frame
     ids = np.full((n, max_bounces), -2, np.int32) if record else None
     ftie = np.zeros(n, np.int32) if record else None
     pos = _c(src_pos, np.float64)
+    er = np.zeros(max(er_capacity, 1), ER_DTYPE)
+    er_n = np.zeros(1, np.int64)
     lib().efo_trace(scene._h, ctypes.byref(cfg), src_key, _p(pos), _p(rays), ray0, n,
-                    _p(H), _p(Dir), _p(st), _p(sum_t), _p(nseg), _p(ids), _p(ftie))
+                    _p(H), _p(Dir), _p(st), _p(sum_t), _p(nseg), _p(ids), _p(ftie),
+                    _p(er), er_capacity, _p(er_n))
     return OracleTrace(H, Dir, dict(zip(ST_NAMES, (int(x) for x in st))), float(sum_t[0]),
-                       nseg, ids, ftie)
+                       nseg, ids, ftie, er[:min(int(er_n[0]), er_capacity)])

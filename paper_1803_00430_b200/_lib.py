@@ -36,7 +36,14 @@ class TraceConfig(ctypes.Structure):
                 ("mode", ctypes.c_int32), ("bin_len", ctypes.c_double),
                 ("listener", ctypes.c_double * 3), ("radius", ctypes.c_double),
                 ("e0", ctypes.c_float), ("record_ids", ctypes.c_int32),
-                ("clear_outputs", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("clear_outputs", ctypes.c_int32), ("diffuse_rain", ctypes.c_int32),
+                ("er_max_order", ctypes.c_int32), ("er_capacity", ctypes.c_int64),
+                ("er_entries", ctypes.c_void_p), ("er_count", ctypes.c_void_p)]
+
+
+# ef_er_entry (72 bytes)
+ER_DTYPE = np.dtype([("src", "<i4"), ("order", "<i4"), ("tri0", "<i4"), ("tri1", "<i4"),
+                     ("dist", "<f8"), ("dir", "<f4", 3), ("pad", "<f4"), ("energy", "<f4", 8)])
 
 
 class AnalysisConfig(ctypes.Structure):

@@ -312,7 +312,8 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max, const float4* s_nodes, int n_smem,
                                            uint32_t& n_nodes, uint32_t& n_tris,
-                                           uint2* s_stack = nullptr, int s_depth = 0) {
+                                           uint2* s_stack = nullptr, int s_depth = 0,
+                                           bool any_hit = false) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
@@ -381,6 +382,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
         EF_PHASE_T0(tl);
         leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
         EF_PHASE_ADD(1, tl);
+        if (any_hit && h.id != INT32_MAX) return h;   // shadow rays: any blocker will do
         EF_PHASE_T0(tp);
         for (;;) {
             if (st.sp == 0) return h;

@@ -70,6 +70,7 @@ struct ef_scene {
     float* fd = nullptr;               // (n_mat, n_bands) diffuse reflection factor
     float* fs = nullptr;               // (n_mat, n_bands) specular reflection factor
     double* pdiff = nullptr;           // (n_mat) probability of a diffuse bounce
+    float* fr = nullptr;               // (n_mat, n_bands) (1 - a) * s for diffuse rain
 };
 
 // error plumbing (ef_api.cpp)

@@ -33,6 +33,7 @@ void free_scene(ef_scene* s) {
     cudaFree(s->fd);
     cudaFree(s->fs);
     cudaFree(s->pdiff);
+    cudaFree(s->fr);
     delete s;
 }
 
@@ -71,7 +72,7 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
     try {
         // material reflection factors: p = mean_b(s_b) summed
         // sequentially; E_b *= (1 - a_b) * s_b/p (diffuse) or (1-s_b)/(1-p)
-        std::vector<float> fd((size_t)n_materials * n_bands), fs(fd.size());
+        std::vector<float> fd((size_t)n_materials * n_bands), fs(fd.size()), fr(fd.size());
         std::vector<double> pd(n_materials);
         for (int m = 0; m < n_materials; ++m) {
             double p = 0.0;
@@ -83,6 +84,7 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
                 const double sb = scattering[m * n_bands + b];
                 fd[m * n_bands + b] = p > 0.0 ? (float)(keep * (sb / p)) : 0.0f;
                 fs[m * n_bands + b] = p < 1.0 ? (float)(keep * ((1.0 - sb) / (1.0 - p))) : 0.0f;
+                fr[m * n_bands + b] = (float)(keep * sb);
             }
         }
         cudaError_t e = cudaSuccess;
@@ -91,6 +93,7 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
         EF_UP(fd, fd.data(), fd.size());
         EF_UP(fs, fs.data(), fs.size());
         EF_UP(pdiff, pd.data(), pd.size());
+        EF_UP(fr, fr.data(), fr.size());
         if (n_tri > 0) {
             HostBvh bvh;
             build_bvh(v0, e1, e2, n_tri, bvh);

@@ -77,6 +77,12 @@ struct TraceParams {
     unsigned long long* counter;
     unsigned long long total;
     int32_t n_smem_nodes;   // BVH nodes [0, n) staged in shared memory
+    int32_t rain;           // diffuse rain (next-event estimation)
+    const float* fr;        // (n_mat, nb) diffusely reflected fraction (1-a)*s, f32
+    int32_t er_max_order;   // arrivals of order 1..er_max_order -> ER list
+    ef_er_entry* er;        // ER list (capacity er_cap), er_count = used entries
+    unsigned int* er_count;
+    int64_t er_cap;
     int32_t timing;         // debug: path_ids rows get (t0, t1, smid, nseg)
 };
 
@@ -103,6 +109,60 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats
 #pragma unroll
     for (int i = 0; i < EF_ST_COUNT; ++i) ls.c[i] = 0;
     ls.sum_t = 0.0;
+}
+
+// One listener arrival of order `order` (reflections before it) at path
+// length `dist` from arrival direction (ux,uy,uz) with per-band energies c[]:
+// order 0 -> Dir, 1..er_max_order -> early-reflection list (when enabled),
+// otherwise the SH histogram bin of dist.
+template <int NBMAX, int ORDER>
+__device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, int order, int tri0,
+                                               int tri1, double dist, double ux, double uy, double uz,
+                                               const float* c, LaneStats& ls) {
+    constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    const int nb = P.nb;
+    ls.c[EF_ST_ARRIVALS]++;
+    float* dst = nullptr;
+    if (order == 0) {
+        ls.c[EF_ST_DIRECT]++;
+        dst = P.Dir + (size_t)src * nb * NK;
+    } else if (order <= P.er_max_order) {
+        const unsigned int slot = atomicAdd(P.er_count, 1u);
+        if (slot < (unsigned int)P.er_cap) {
+            ef_er_entry& e = P.er[slot];
+            e.src = src;
+            e.order = order;
+            e.tri0 = tri0;
+            e.tri1 = tri1;
+            e.dist = dist;
+            e.dir[0] = (float)ux;
+            e.dir[1] = (float)uy;
+            e.dir[2] = (float)uz;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) e.energy[b] = b < nb ? c[b] : 0.f;
+        }
+        return;
+    } else {
+        const double q = dist / P.bin_len;
+        if (q < (double)P.n_bins)
+            dst = P.H + ((size_t)src * P.n_bins + (size_t)q) * nb * NK;
+        else
+            ls.c[EF_ST_DROPPED]++;
+    }
+    if (dst) {
+        double Y[NK];
+        eval_sh<ORDER>(ux, uy, uz, Y);
+        float Yf[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
+#pragma unroll
+        for (int b = 0; b < NBMAX; ++b) {
+            if (b < nb) {
+#pragma unroll
+                for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, c[b] * Yf[k]);
+            }
+        }
+    }
 }
 
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
@@ -139,6 +199,8 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     for (int b = 0; b < NBMAX; ++b) E[b] = 0.f;
     uint32_t ray = 0, skey = 0;
     int src = 0, nrefl = 0, nseg = 0;
+    int tri0 = -1, tri1 = -1;
+    bool last_diffuse = false;
     unsigned long long path = 0;
     unsigned long long t_start = 0;
 
@@ -169,6 +231,8 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                     plen = 0.0;
                     nrefl = 0;
                     nseg = 0;
+                    tri0 = tri1 = -1;
+                    last_diffuse = false;
                     if (src != ls.src) {
                         flush_stats(ls, s_stats, s_sumt);
                         ls.src = src;
@@ -196,42 +260,19 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         EF_PHASE_T0(tsh);
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
-        // ---- listener sphere receiver + SH histogram commit
-        {
+        // ---- listener sphere receiver + SH histogram commit (with diffuse
+        // rain, segments leaving a diffuse bounce reach the listener only
+        // through the next-event connection: SPEC.md:257, no double count)
+        if (!(P.rain && last_diffuse)) {
             const double Lx = P.lx - ox, Ly = P.ly - oy, Lz = P.lz - oz;
             const double tc = dot3(Lx, Ly, Lz, dx, dy, dz);
             const double tlim = hit ? h.t : INFINITY;
             if (tc > 0.0 && tc < tlim) {
                 const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
                 const double perp2 = dist2 - tc * tc;
-                if (perp2 <= P.r2) {
-                    float* dst = nullptr;
-                    ls.c[EF_ST_ARRIVALS]++;
-                    if (nrefl == 0) {
-                        ls.c[EF_ST_DIRECT]++;
-                        dst = P.Dir + (size_t)src * nb * NK;
-                    } else {
-                        const double q = (plen + tc) / P.bin_len;
-                        if (q < (double)P.n_bins)
-                            dst = P.H + ((size_t)src * P.n_bins + (size_t)q) * nb * NK;
-                        else
-                            ls.c[EF_ST_DROPPED]++;
-                    }
-                    if (dst) {
-                        double Y[NK];
-                        eval_sh<ORDER>(-dx, -dy, -dz, Y);
-                        float Yf[NK];
-#pragma unroll
-                        for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
-#pragma unroll
-                        for (int b = 0; b < NBMAX; ++b) {
-                            if (b < nb) {
-#pragma unroll
-                                for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, E[b] * Yf[k]);
-                            }
-                        }
-                    }
-                }
+                if (perp2 <= P.r2)
+                    commit_arrival<NBMAX, ORDER>(P, src, nrefl, tri0, tri1, plen + tc, -dx, -dy, -dz,
+                                                 E, ls);
             }
         }
         ++nseg;
@@ -248,6 +289,8 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             oy = oy + t * dy;
             oz = oz + t * dz;
             ++nrefl;
+            if (nrefl == 1) tri0 = h.id;
+            if (nrefl == 2) tri1 = h.id;
             ls.c[EF_ST_REFLECTIONS]++;
             const int m = __ldg(P.mat + h.id);
             const double nx = __ldg(P.normals + 3 * h.id + 0);
@@ -256,11 +299,43 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             double u1, u2;
             draw2(ray, (uint32_t)nrefl, 0u, P.frame, P.seed, skey, u1, u2);
             const bool diffuse = u1 < __ldg(P.pdiff + m);
+            const double nd = dot3(nx, ny, nz, dx, dy, dz);
+            if (P.rain && diffuse) {
+                // ---- diffuse rain: connect this bounce to the listener
+                // centre; Lambertian lobe through the receiver cross-section:
+                // c_b = E_b (1-a_b) s_b cos(theta) r^2 / d^2
+                const double sg = nd > 0.0 ? -1.0 : 1.0;   // normal facing the incoming side
+                const double Lx = P.lx - ox, Ly = P.ly - oy, Lz = P.lz - oz;
+                const double d2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
+                const double dd = sqrt(d2);
+                const double cosv = dot3(sg * nx, sg * ny, sg * nz, Lx, Ly, Lz) / dd;
+                if (cosv > 0.0 && dd > kRayEps) {
+                    const double ex = Lx / dd, ey = Ly / dd, ez = Lz / dd;
+                    const double limit = dd - kRayEps;
+                    Hit sh;
+                    if (BRUTE) {
+                        sh = closest_brute(s_tri, P.n_tri, ox, oy, oz, ex, ey, ez, kRayEps, limit);
+                    } else {
+                        sh = closest_bvh(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit, s_nodes,
+                                         P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
+                                         s_stack + threadIdx.x, smem_stack_depth<THREADS>(), true);
+                    }
+                    if (sh.id == INT32_MAX) {
+                        const float gf = (float)(cosv * P.r2 / d2);
+                        float c[NBMAX];
+#pragma unroll
+                        for (int b = 0; b < NBMAX; ++b)
+                            c[b] = b < nb ? E[b] * __ldg(P.fr + m * nb + b) * gf : 0.f;
+                        commit_arrival<NBMAX, ORDER>(P, src, nrefl, tri0, tri1, plen + dd, -ex, -ey,
+                                                     -ez, c, ls);
+                    }
+                }
+            }
+            last_diffuse = diffuse;
             const float* f = (diffuse ? P.fd : P.fs) + m * nb;
 #pragma unroll
             for (int b = 0; b < NBMAX; ++b)
                 if (b < nb) E[b] = E[b] * __ldg(f + b);
-            const double nd = dot3(nx, ny, nz, dx, dy, dz);
             if (diffuse) {
                 const double s = nd > 0.0 ? -1.0 : 1.0;
                 sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny, s * nz,
@@ -547,6 +622,8 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
     if (!(cfg->bin_len > 0.0) || !(cfg->radius >= 0.0))
         return set_error(EF_EINVAL, "ef_trace: bin_len must be > 0 and radius >= 0");
     if (cfg->mode < 0 || cfg->mode > 2) return set_error(EF_EINVAL, "ef_trace: mode must be 0, 1 or 2");
+    if (cfg->er_entries && (!cfg->er_count || cfg->er_capacity < 0))
+        return set_error(EF_EINVAL, "ef_trace: an early-reflection list needs er_count and er_capacity >= 0");
     if (!src_pos || !H || !Dir || !stats || !sum_t) return set_error(EF_EINVAL, "ef_trace: null buffer");
     if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_trace: empty scene is handled by the host");
     const bool brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= kBruteMaxTris);
@@ -604,6 +681,12 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
         P.path_ids = (path_ids && cfg->record_ids) ? path_ids + (size_t)s0 * cfg->n_rays * cfg->max_bounces : nullptr;
         P.timing = (P.path_ids && cfg->record_ids == 2 && cfg->max_bounces >= 6) ? 1 : 0;
+        P.rain = cfg->diffuse_rain ? 1 : 0;
+        P.fr = s->fr;
+        P.er_max_order = cfg->er_entries ? std::max(0, std::min(cfg->er_max_order, 2)) : 0;
+        P.er = static_cast<ef_er_entry*>(cfg->er_entries);
+        P.er_count = cfg->er_count;
+        P.er_cap = cfg->er_capacity;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
         P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, kNodeCacheBytes / sizeof(GpuNode));

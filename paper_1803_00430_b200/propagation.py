@@ -37,6 +37,9 @@ class TraceConfig:
     seed: int = 0
     mode: int = 0                       # 0 reference dispatch, 1 all-pairs, 2 BVH
     max_rt: float | None = None         # RT60 clamp (default: IR length)
+    diffuse_rain: bool = False          # next-event connection per diffuse bounce
+    er_max_order: int = 0               # arrivals of order 1..er_max_order -> PathList (<= 2)
+    er_capacity: int = 1 << 20          # device ER list entries per launch
 
     @property
     def n_coeffs(self) -> int:
@@ -91,12 +94,48 @@ class TraceStats:
 
 @dataclass
 class PathList:
-    """Early-reflection paths.  ER extraction is the first
-    'next' item of SURVEY.md 8(f); this build routes all energy to the IR."""
-    delays: list = field(default_factory=list)
-    pressures: list = field(default_factory=list)
-    directivities: list = field(default_factory=list)
+    """Early-reflection paths: one entry per distinct
+    (source, reflection order, reflecting triangles) sequence of the frame's
+    order <= er_max_order arrivals; delay = energy-weighted path length / c,
+    pressure_b = sqrt(energy_b), directivity = energy-weighted order-2 SH of
+    the arrival directions.  Empty unless enabled."""
+    delays: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    pressures: np.ndarray = field(default_factory=lambda: np.zeros((0, 4)))
+    directivities: np.ndarray = field(default_factory=lambda: np.zeros((0, 9)))
     kinds: list = field(default_factory=list)
+    sources: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    orders: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    triangles: np.ndarray = field(default_factory=lambda: np.zeros((0, 2), np.int64))
+    dropped: int = 0
+
+    def __len__(self) -> int:
+        return len(self.delays)
+
+
+def build_path_list(entries: np.ndarray, n_bands: int, speed_of_sound: float,
+                    dropped: int = 0) -> PathList:
+    """Group raw ER arrivals (ef_er_entry records) by reflection sequence."""
+    from .sh import eval_sh_batch
+    if len(entries) == 0:
+        return PathList(pressures=np.zeros((0, n_bands)), dropped=dropped)
+    key = np.stack([entries["src"], entries["order"], entries["tri0"], entries["tri1"]], 1)
+    uniq, inv = np.unique(key, axis=0, return_inverse=True)
+    inv = inv.reshape(-1)
+    e = entries["energy"][:, :n_bands].astype(np.float64)
+    etot = e.sum(1)
+    g = len(uniq)
+    esum = np.zeros((g, n_bands))
+    np.add.at(esum, inv, e)
+    wsum = np.bincount(inv, weights=etot, minlength=g)
+    dist = np.bincount(inv, weights=etot * entries["dist"], minlength=g) / np.maximum(wsum, 1e-300)
+    Y = eval_sh_batch(entries["dir"].astype(np.float64), 2)
+    ysum = np.zeros((g, 9))
+    np.add.at(ysum, inv, Y * etot[:, None])
+    return PathList(delays=dist / speed_of_sound, pressures=np.sqrt(esum),
+                    directivities=ysum / np.maximum(wsum, 1e-300)[:, None],
+                    kinds=["early-reflection"] * g, sources=uniq[:, 0].astype(np.int64),
+                    orders=uniq[:, 1].astype(np.int64), triangles=uniq[:, 2:].astype(np.int64),
+                    dropped=dropped)
 
 
 @dataclass
@@ -138,6 +177,11 @@ class FrameTracer:
         self.record = record
         self.path_nseg = None
         self.path_ids = None
+        self.er = None
+        self.er_count = None
+        if config.er_max_order > 0:
+            self.er = t.zeros((config.er_capacity * _lib.ER_DTYPE.itemsize,), dtype=t.uint8, device=dev)
+            self.er_count = t.zeros((1,), dtype=t.int32, device=dev)
         self._handle = scene._device_handle()
 
     def set_sources(self, positions, keys=None):
@@ -180,6 +224,14 @@ class FrameTracer:
         cfg.e0 = c.e0(total_rays)
         cfg.record_ids = int(self.record)
         cfg.clear_outputs = int(bool(clear))
+        cfg.diffuse_rain = int(bool(c.diffuse_rain))
+        if self.er is not None:
+            if clear:
+                self.er_count.zero_()
+            cfg.er_max_order = min(int(c.er_max_order), 2)
+            cfg.er_capacity = int(c.er_capacity)
+            cfg.er_entries = self.er.data_ptr()
+            cfg.er_count = self.er_count.data_ptr()
         self.path_nseg = self.path_ids = None
         if self.record:
             self.path_nseg = t.zeros((self.n_sources, n_rays), dtype=t.int32, device=self.H.device)
@@ -189,6 +241,19 @@ class FrameTracer:
             self._handle, cfg, _lib.ptr(self.src_pos), _lib.ptr(self.src_key), _lib.ptr(ids),
             _lib.ptr(self.H), _lib.ptr(self.Dir), _lib.ptr(self.stats), _lib.ptr(self.sum_t),
             _lib.ptr(self.path_nseg), _lib.ptr(self.path_ids), _lib.stream_handle(stream)))
+
+    def early_reflections(self) -> np.ndarray:
+        """Raw ER arrivals of the last trace (structured ef_er_entry array)."""
+        if self.er is None:
+            return np.zeros(0, _lib.ER_DTYPE)
+        n = min(int(self.er_count.item()), self.config.er_capacity)
+        return self.er[:n * _lib.ER_DTYPE.itemsize].cpu().numpy().view(_lib.ER_DTYPE).copy()
+
+    def path_list(self) -> PathList:
+        n_total = 0 if self.er is None else int(self.er_count.item())
+        raw = self.early_reflections()
+        return build_path_list(raw, self.nb, self.scene.speed_of_sound,
+                               dropped=max(0, n_total - self.config.er_capacity))
 
     def irs(self):
         return [LowRateIR(1.0 / self.config.bin_s, self.H[s], self.Dir[s]) for s in range(self.n_sources)]
@@ -229,7 +294,8 @@ def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceC
     if caches is not None and dt is not None:
         ir = accumulate_ir(caches.ir.get(key), ir, caches.tau_lr, dt)
         caches.ir[key] = ir
-    return PathList(), ir, tr.trace_stats()[0]
+    paths = tr.path_list() if cfg.er_max_order > 0 else PathList()
+    return paths, ir, tr.trace_stats()[0]
 
 
 def accumulate_ir(cache_ir: LowRateIR | None, frame_ir: LowRateIR, tau: float, dt: float) -> LowRateIR:

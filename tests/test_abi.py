@@ -58,7 +58,9 @@ def test_scene_create_validates_before_cuda():
 
 def test_trace_config_layout_matches_header():
     # ef_trace_config: 4*i32, i64, 3*u32, i32, f64, 3*f64, f64, f32, i32
-    assert ctypes.sizeof(_lib.TraceConfig) == 96
+    assert ctypes.sizeof(_lib.TraceConfig) == 128
+    assert _lib.TraceConfig.er_capacity.offset == 104
+    assert _lib.ER_DTYPE.itemsize == 72
     assert _lib.TraceConfig.n_rays.offset == 16
     assert _lib.TraceConfig.bin_len.offset == 40
     assert _lib.TraceConfig.e0.offset == 80

@@ -471,3 +471,48 @@ def test_c4_crossover_and_constant_cost_properties():
     np.testing.assert_allclose(sos, np.array(OA4.band_sos())[:, :, [0, 1, 2, 4, 5]], rtol=1e-6, atol=1e-7)
     p = workloads.c4_params(n_sources=2)
     assert p["hrtf"].shape == (16, 2, 256)   # 16 SH channels x 2 ears = 32 filters
+
+
+# ---------------------------------------- rain + ER paths
+@pytest.mark.parametrize("name,n", [("c1", 1024), ("c2", 2048)])
+def test_diffuse_rain_and_early_reflections(name, n):
+    """Diffuse rain (next-event estimation from every diffuse bounce) and
+    order <= 2 arrivals routed to the early-reflection list: device vs the
+    C oracle on the same rays -- identical arrival counts, histogram within
+    1e-4, ER energies per reflection sequence within 1e-5."""
+    w = workloads.WORKLOADS[name]()
+    sc = scene.scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius,
+                                  seed=w.seed, diffuse_rain=True, er_max_order=2,
+                                  er_capacity=1 << 18)
+    tr = propagation.FrameTracer(sc, 1, cfg, record=True)
+    tr.set_sources(w.sources[:1], [0])
+    tr.trace(w.listener, n_rays=n)
+    torch.cuda.synchronize()
+    os_ = _oracle_for(w)
+    ref = O.trace(os_, src_key=0, src_pos=w.sources[0], listener=w.listener, radius=w.radius,
+                  seed=w.seed, order=w.order, n_bins=w.n_bins, bin_len=w.speed_of_sound * w.bin_s,
+                  max_bounces=w.max_bounces, e0=cfg.e0(), n_rays=n, record=True, rain=True,
+                  er_max_order=2, er_capacity=1 << 18)
+    if (ref.first_tie >= 0).any():
+        pytest.skip("near-tie path in the subsample")
+    st = tr.trace_stats()[0]
+    assert st.arrivals == ref.stats["arrivals"] and st.arrivals > 0
+    assert st.total_segments == ref.stats["segments"]
+    _hist_close(tr.H[0].cpu().numpy(), ref.H)
+    g = tr.early_reflections()
+    assert len(g) == len(ref.er) > 0
+    def groups(er):
+        out = {}
+        for e in er:
+            k = (int(e["order"]), int(e["tri0"]), int(e["tri1"]))
+            out[k] = out.get(k, 0.0) + e["energy"][:w.n_bands].astype(np.float64)
+        return out
+    gg, gr = groups(g), groups(ref.er)
+    assert gg.keys() == gr.keys()
+    for k in gr:
+        np.testing.assert_allclose(gg[k], gr[k], rtol=1e-5, atol=1e-12)
+    pl = tr.path_list()
+    assert len(pl) == len(gr) and np.all(pl.delays > 0) and set(pl.orders) <= {1, 2}
+    assert np.all(pl.pressures >= 0) and pl.directivities.shape[1] == 9
