@@ -309,3 +309,53 @@ def accumulate_ir(cache_ir: LowRateIR | None, frame_ir: LowRateIR, tau: float, d
     return LowRateIR(frame_ir.sample_rate,
                      blend_histograms(cache_ir.histogram, frame_ir.histogram, a),
                      blend_histograms(cache_ir.direct, frame_ir.direct, a))
+
+
+def compute_direct_sound(scene, source, listener, rng=None, samples: int = 64, order: int = 3,
+                         power: float = 1.0, t: float = 0.0) -> PathList:
+    """Direct path entry.  Point source (radius 0): one
+    visibility ray; intensity P/(4 pi d^2), directivity Y(direction to the
+    source).  Spherical source: `samples` directions uniform in the cone it
+    subtends, each tested for visibility (ef_occluded_batch); the entry
+    carries the visible fraction of the intensity and the mean SH projection
+    of the visible directions.  A fully occluded source yields pressure 0."""
+    from .sh import eval_sh_batch
+    sp = np.asarray(source.pose_at(t) if hasattr(source, "pose_at") else source, np.float64)
+    lp = np.asarray(listener.pose_at(t)[0] if hasattr(listener, "pose_at") else listener, np.float64)
+    radius = float(getattr(source, "radius", 0.0))
+    gain = float(getattr(source, "gain", 1.0))
+    v = sp - lp
+    dist = float(np.linalg.norm(v))
+    if dist <= 0.0:
+        raise ValueError("source and listener coincide")
+    axis = v / dist
+    intensity = power * gain * gain / (4.0 * np.pi * dist * dist)
+    nb = scene.n_bands
+    if radius <= 0.0 or radius >= dist:
+        dirs = axis[None, :]
+        targets = sp[None, :]
+    else:
+        rng = np.random.default_rng(rng)
+        cos_max = np.sqrt(1.0 - (radius / dist) ** 2)
+        z = rng.uniform(cos_max, 1.0, samples)
+        phi = rng.uniform(0.0, 2.0 * np.pi, samples)
+        r = np.sqrt(1.0 - z * z)
+        # orthonormal basis around the axis (Duff et al.)
+        sg = np.copysign(1.0, axis[2])
+        a = -1.0 / (sg + axis[2])
+        b = axis[0] * axis[1] * a
+        t1 = np.array([1.0 + sg * axis[0] * axis[0] * a, sg * b, -sg * axis[0]])
+        t2 = np.array([b, sg + axis[1] * axis[1] * a, -axis[1]])
+        dirs = (r * np.cos(phi))[:, None] * t1 + (r * np.sin(phi))[:, None] * t2 + z[:, None] * axis
+        # target: where the direction meets the source sphere (near side)
+        tc = dirs @ v
+        disc = np.maximum(tc * tc - (dist * dist - radius * radius), 0.0)
+        targets = lp + (tc - np.sqrt(disc))[:, None] * dirs
+    blocked = scene.occluded_batch(np.repeat(lp[None, :], len(dirs), axis=0), targets)
+    vis = ~np.asarray(blocked)
+    frac = float(vis.mean())
+    Y = eval_sh_batch(dirs[vis], order).mean(axis=0) if vis.any() else np.zeros((order + 1) ** 2)
+    p = np.sqrt(intensity * frac)
+    return PathList(delays=np.array([dist / scene.speed_of_sound]), pressures=np.full((1, nb), p),
+                    directivities=Y[None, :], kinds=["direct"], sources=np.array([0]),
+                    orders=np.array([0]), triangles=np.full((1, 2), -1))

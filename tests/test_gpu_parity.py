@@ -522,3 +522,24 @@ def test_diffuse_rain_and_early_reflections(name, n):
     pl = tr.path_list()
     assert len(pl) == len(gr) and np.all(pl.delays > 0) and set(pl.orders.tolist()) <= {1, 2}
     assert np.all(pl.pressures >= 0) and pl.directivities.shape[1] == 9
+
+
+def test_compute_direct_sound_spec_examples():
+    """point source 2 m away, unoccluded -> intensity
+    P/(4 pi 4) and dominant direction = direction to the source (1e-3); fully
+    behind a wall -> zero entry; spherical source radius 1 m at 2 m -> positive
+    l=0 and dominant direction within the 30 degree angular radius."""
+    box = scene.make_box_scene(size=10.0)
+    src = scene.Source(id="s", position=np.array([2.0, 0.0, 0.0]))
+    lst = scene.Listener(position=np.zeros(3))
+    pl = propagation.compute_direct_sound(box, src, lst)
+    assert abs(pl.pressures[0, 0] ** 2 - 1.0 / (4 * np.pi * 4)) < 1e-12
+    dd = sh.dominant_direction(pl.directivities[0])
+    assert np.abs(dd - np.array([1.0, 0, 0])).max() < 1e-3
+    hidden = scene.Source(id="h", position=np.array([7.0, 0.0, 0.0]))    # outside the box
+    assert propagation.compute_direct_sound(box, hidden, lst).pressures[0, 0] == 0.0
+    big = scene.Source(id="b", position=np.array([0.0, 2.0, 0.0]), radius=1.0)
+    pl = propagation.compute_direct_sound(box, big, lst, rng=1, samples=512)
+    assert pl.directivities[0, 0] > 0
+    dd = sh.dominant_direction(pl.directivities[0])
+    assert np.degrees(np.arccos(np.clip(dd @ np.array([0, 1.0, 0]), -1, 1))) < 30.0
