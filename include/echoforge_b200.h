@@ -96,6 +96,12 @@ int ef_scene_create(const double* v0, const double* e1, const double* e2,
                     const double* absorption, const double* scattering,
                     int32_t n_materials, int32_t n_bands, ef_scene** out);
 int ef_scene_destroy(ef_scene* scene);
+/* Dynamic geometry: replace the triangle
+ * data of a scene (same triangle count and ids; DEVICE v0/e1/e2/normals
+ * (n_tri,3) f64) and refit the device BVH bottom-up, one kernel per level.
+ * Stream-ordered; the tree topology is kept, boxes stay conservative. */
+int ef_scene_refit(ef_scene* scene, const double* v0, const double* e1, const double* e2,
+                   const double* normals, void* stream);
 /* out[0]=n_tri out[1]=n_nodes out[2]=max_depth out[3]=device bytes
  * out[4]=max leaf size out[5]=n_bands out[6]=n_materials */
 int ef_scene_info(const ef_scene* scene, int64_t* out7);

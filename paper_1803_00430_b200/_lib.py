@@ -56,7 +56,8 @@ class AnalysisConfig(ctypes.Structure):
 EXPORTS = ("ef_abi_version", "ef_last_error", "ef_launch_count", "ef_scene_create",
            "ef_scene_destroy", "ef_scene_info", "ef_intersect_batch", "ef_occluded_batch",
            "ef_ray_triangles", "ef_eval_sh_batch", "ef_loudness_batch", "ef_trace", "ef_analyze", "ef_blend",
-           "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process")
+           "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process",
+           "ef_scene_refit")
 
 
 def lib():
@@ -87,6 +88,7 @@ def lib():
                              vp, vp, vp, vp]
     L.ef_blend.argtypes = [vp, vp, i64, f64, vp, vp]
     L.ef_audio_create.argtypes = [vp] * 13
+    L.ef_scene_refit.argtypes = [vp] * 6
     L.ef_audio_destroy.argtypes = [vp]
     L.ef_audio_info.argtypes = [vp, vp]
     L.ef_audio_process.argtypes = [vp, vp, vp, vp, vp]

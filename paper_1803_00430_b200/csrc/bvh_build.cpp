@@ -253,6 +253,9 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
         out.nodes.push_back(g);
         out.max_depth = 1;
         out.max_stack = 1;
+        out.pad = pad;
+        out.level_nodes.assign(1, 0);
+        out.level_start = {0, 1};
         return;
     }
     struct Item { int32_t bn; int32_t slot; int depth; };
@@ -298,6 +301,21 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
     }
     out.max_depth = max_depth;
     out.max_stack = 3 * max_depth + 1;   // at most three pushes per level
+    out.pad = pad;
+    // depth of every node (children are allocated after their parent)
+    std::vector<int> depth(out.nodes.size(), 0);
+    for (size_t i = 0; i < out.nodes.size(); ++i)
+        for (int c = 0; c < 4; ++c) {
+            const int32_t ch = out.nodes[i].child[c];
+            if (ch >= 0) depth[ch] = depth[i] + 1;
+        }
+    std::vector<std::vector<int32_t>> lv(max_depth);
+    for (size_t i = 0; i < out.nodes.size(); ++i) lv[depth[i]].push_back((int32_t)i);
+    out.level_start.assign(1, 0);
+    for (auto& l : lv) {
+        out.level_nodes.insert(out.level_nodes.end(), l.begin(), l.end());
+        out.level_start.push_back((int64_t)out.level_nodes.size());
+    }
 }
 
 }  // namespace ef

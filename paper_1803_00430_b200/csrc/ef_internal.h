@@ -41,6 +41,9 @@ static_assert(sizeof(GpuTri) == 80, "tri must be 80 bytes");
 
 struct HostBvh {
     std::vector<GpuNode> nodes;
+    std::vector<int32_t> level_nodes;   // node indices grouped by depth (root level first)
+    std::vector<int64_t> level_start;   // offsets into level_nodes, size levels + 1
+    double pad = 0.0;                   // absolute box padding used by the build
     std::vector<int64_t> order;  // leaf-order position -> original triangle id
     int max_depth = 0;           // of the 4-wide tree
     int max_leaf = 0;
@@ -71,6 +74,11 @@ struct ef_scene {
     float* fs = nullptr;               // (n_mat, n_bands) specular reflection factor
     double* pdiff = nullptr;           // (n_mat) probability of a diffuse bounce
     float* fr = nullptr;               // (n_mat, n_bands) (1 - a) * s for diffuse rain
+    // refit support (dynamic scenes)
+    int64_t* leaf_order = nullptr;     // (n_tri) leaf position -> original id
+    int32_t* level_nodes = nullptr;    // node indices grouped by depth
+    std::vector<int64_t> level_start;  // host copy of the level offsets
+    double pad = 0.0;
 };
 
 // error plumbing (ef_api.cpp)

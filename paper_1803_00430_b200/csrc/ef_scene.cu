@@ -3,6 +3,7 @@
 // scene.py:149-171; SceneModel is immutable after construction).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <exception>
 #include <string>
@@ -34,6 +35,8 @@ void free_scene(ef_scene* s) {
     cudaFree(s->fs);
     cudaFree(s->pdiff);
     cudaFree(s->fr);
+    cudaFree(s->leaf_order);
+    cudaFree(s->level_nodes);
     delete s;
 }
 
@@ -125,6 +128,10 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
                 return set_error(EF_EUNSUPPORTED, "ef_scene_create: BVH deeper than the traversal stack");
             }
             EF_UP(nodes, bvh.nodes.data(), bvh.nodes.size());
+            EF_UP(leaf_order, bvh.order.data(), bvh.order.size());
+            EF_UP(level_nodes, bvh.level_nodes.data(), bvh.level_nodes.size());
+            s->level_start = bvh.level_start;
+            s->pad = bvh.pad;
             EF_UP(tris, tris.data(), tris.size());
             EF_UP(tris_by_id, by_id.data(), by_id.size());
             EF_UP(normals, normals, (size_t)3 * n_tri);
@@ -158,4 +165,94 @@ extern "C" int ef_scene_info(const ef_scene* s, int64_t* o) {
     o[5] = s->n_bands;
     o[6] = s->n_mat;
     return EF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Dynamic scenes: new vertex data for the same triangle
+// list, then a bottom-up refit of the 4-wide tree on the device, one launch
+// per tree level (deepest first).  Topology and leaf order are kept.
+namespace {
+
+__global__ void update_tris_kernel(ef::GpuTri* tris, double* by_id, double* normals_out,
+                                   const int64_t* order, const double* v0, const double* e1,
+                                   const double* e2, const double* normals, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t id = order[i];
+        ef::GpuTri t;
+        for (int k = 0; k < 3; ++k) {
+            t.v[k] = v0[3 * id + k];
+            t.v[3 + k] = e1[3 * id + k];
+            t.v[6 + k] = e2[3 * id + k];
+        }
+        t.id = id;
+        tris[i] = t;
+        for (int k = 0; k < 3; ++k) {
+            by_id[9 * i + k] = v0[3 * i + k];
+            by_id[9 * i + 3 + k] = e1[3 * i + k];
+            by_id[9 * i + 6 + k] = e2[3 * i + k];
+            normals_out[3 * i + k] = normals[3 * i + k];
+        }
+    }
+}
+
+__global__ void refit_level_kernel(ef::GpuNode* nodes, const ef::GpuTri* tris,
+                                   const int32_t* level, int64_t count, double pad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        ef::GpuNode& g = nodes[level[i]];
+        for (int c = 0; c < 4; ++c) {
+            const int32_t ch = g.child[c];
+            if (ch == ef::kEmptyChild) continue;
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            if (ch >= 0) {   // inner child: union of its (already refit) slots
+                const ef::GpuNode& cn = nodes[ch];
+                for (int k = 0; k < 4; ++k) {
+                    if (cn.child[k] == ef::kEmptyChild) continue;
+                    lo[0] = fmin(lo[0], (double)cn.lox[k]); hi[0] = fmax(hi[0], (double)cn.hix[k]);
+                    lo[1] = fmin(lo[1], (double)cn.loy[k]); hi[1] = fmax(hi[1], (double)cn.hiy[k]);
+                    lo[2] = fmin(lo[2], (double)cn.loz[k]); hi[2] = fmax(hi[2], (double)cn.hiz[k]);
+                }
+                // already padded and rounded outward one level down
+                g.lox[c] = (float)lo[0]; g.hix[c] = (float)hi[0];
+                g.loy[c] = (float)lo[1]; g.hiy[c] = (float)hi[1];
+                g.loz[c] = (float)lo[2]; g.hiz[c] = (float)hi[2];
+            } else {         // leaf: vertices v0, v0+e1, v0+e2 of its triangles
+                const uint32_t e = ~(uint32_t)ch;
+                const uint32_t start = e >> 3, cnt = (e & 7u) + 1u;
+                for (uint32_t j = 0; j < cnt; ++j) {
+                    const double* v = tris[start + j].v;
+                    for (int k = 0; k < 3; ++k) {
+                        const double a = v[k], b = v[k] + v[3 + k], d = v[k] + v[6 + k];
+                        lo[k] = fmin(lo[k], fmin(a, fmin(b, d)));
+                        hi[k] = fmax(hi[k], fmax(a, fmax(b, d)));
+                    }
+                }
+                g.lox[c] = __double2float_rd(lo[0] - pad); g.hix[c] = __double2float_ru(hi[0] + pad);
+                g.loy[c] = __double2float_rd(lo[1] - pad); g.hiy[c] = __double2float_ru(hi[1] + pad);
+                g.loz[c] = __double2float_rd(lo[2] - pad); g.hiz[c] = __double2float_ru(hi[2] + pad);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, const double* e2,
+                              const double* normals, void* stream) {
+    if (!s || !v0 || !e1 || !e2 || !normals) return set_error(EF_EINVAL, "ef_scene_refit: null argument");
+    if (s->n_tri == 0) return EF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = s->n_tri;
+    update_tris_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(
+        s->tris, s->tris_by_id, s->normals, s->leaf_order, v0, e1, e2, normals, n);
+    count_launch();
+    const int levels = (int)s->level_start.size() - 1;
+    for (int l = levels - 1; l >= 0; --l) {
+        const int64_t a = s->level_start[l], cnt = s->level_start[l + 1] - a;
+        refit_level_kernel<<<(int)std::min<int64_t>((cnt + 127) / 128, 148 * 8), 128, 0, st>>>(
+            s->nodes, s->tris, s->level_nodes + a, cnt, s->pad);
+        count_launch();
+    }
+    return check_cuda(cudaGetLastError(), "ef_scene_refit");
 }

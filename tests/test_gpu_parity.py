@@ -543,3 +543,33 @@ def test_compute_direct_sound_spec_examples():
     assert pl.directivities[0, 0] > 0
     dd = sh.dominant_direction(pl.directivities[0])
     assert np.degrees(np.arccos(np.clip(dd @ np.array([0, 1.0, 0]), -1, 1))) < 30.0
+
+
+def test_dynamic_refit_matches_rebuild_and_oracle():
+    """move rigid boxes of the C2 city (update_geometry ->
+    device refit of the existing tree) and trace: hit ids and bounce counts
+    equal a fresh build of the moved scene and the oracle (outside near-ties)."""
+    w = workloads.c2_city()
+    sc = scene.scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    tr = propagation.FrameTracer(sc, 1, cfg, record=True)      # builds the original tree
+    tr.set_sources(w.sources[2:3], [2])
+    tr.trace(w.listener, n_rays=64)
+    moved = w.tris.copy()
+    for b in (3, 17, 42, 99):                                    # boxes: 12 triangles each after the ground
+        moved[2 + 12 * b: 2 + 12 * (b + 1)] += np.array([6.0, -4.0, 0.0])
+    A, B, C = moved[:, 0], moved[:, 1], moved[:, 2]
+    sc.update_geometry(A, B - A, C - A)
+    n = 2048
+    tr.trace(w.listener, n_rays=n)
+    torch.cuda.synchronize()
+    w2 = workloads.Workload("moved", moved, w.material_index, w.absorption, w.scattering,
+                            w.sources, w.listener, w.radius, w.n_rays, w.max_bounces, w.order,
+                            seed=w.seed)
+    _, _, fresh = _run_gpu(w2, n_rays=n, sources=[2])
+    assert np.array_equal(tr.path_ids.cpu().numpy(), fresh.path_ids.cpu().numpy())
+    assert np.array_equal(tr.path_nseg.cpu().numpy(), fresh.path_nseg.cpu().numpy())
+    ref = _oracle_trace(_oracle_for(w2), w2, 2, np.arange(n, dtype=np.uint32))
+    bad, excl = _compare_paths(tr.path_nseg.cpu().numpy()[0], tr.path_ids.cpu().numpy()[0], ref)
+    assert bad == 0 and excl <= 0.01 * n
