@@ -221,6 +221,14 @@ int ef_analyze(const ef_analysis_config* cfg, const float* H, const float* Dir,
                int32_t n_design, double* params, double* src_params, double* avg_dir,
                double* loudness, void* stream);
 
+/* Replaces acoustic_metrics: DEVICE
+ * energy (n_series, n_bins) f64 per-bin energy, direct_index (n_series) i32
+ * or NULL (= 0); e_ref = free-field direct energy at 10 m.  out (n_series, 5)
+ * f64 = RT60 (-1 when silent), C80 dB (+99 sentinel), D50, TS s, G dB. */
+int ef_acoustic_metrics(const double* energy, int64_t n_series, int32_t n_bins, double bin_s,
+                        const int32_t* direct_index, double e_ref, double max_rt, double* out,
+                        void* stream);
+
 /* Replaces accumulate_ir: DEVICE f32 arrays of n
  * elements, out = alpha * frame + (1 - alpha) * cache (out may alias). */
 int ef_blend(const float* cache, const float* frame, int64_t n, double alpha, float* out,

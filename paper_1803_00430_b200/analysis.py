@@ -156,3 +156,24 @@ def blend_into(cache, frame, alpha: float):
     _lib.check(_lib.lib().ef_blend(_lib.ptr(cache), _lib.ptr(frame), frame.numel(), float(alpha),
                                    _lib.ptr(cache), _lib.stream_handle()))
     return cache
+
+
+def acoustic_metrics(energy, bin_s: float, direct_index=0, e_ref: float = 1.0 / (4.0 * math.pi * 100.0),
+                     max_rt: float = 8.0) -> dict:
+    """RT60, C80, D50, TS, G per energy series on the
+    device.  ``energy``: (n_bins,) or (n_bins, n_bands) energy per bin
+    (pressure squared); metrics are measured from ``direct_index``; G is
+    relative to ``e_ref`` (direct sound at 10 m in the free field)."""
+    t = _lib.torch()
+    E = np.asarray(energy, dtype=np.float64)
+    single = E.ndim == 1
+    E2 = np.ascontiguousarray((E[:, None] if single else E).T)          # (series, n_bins)
+    dev = _lib.to_device(E2, t.float64)
+    di = _lib.to_device(np.full(E2.shape[0], int(direct_index), np.int32), t.int32)
+    out = t.zeros((E2.shape[0], 5), dtype=t.float64, device=dev.device)
+    _lib.check(_lib.lib().ef_acoustic_metrics(_lib.ptr(dev), E2.shape[0], E2.shape[1], float(bin_s),
+                                              _lib.ptr(di), float(e_ref), float(max_rt), _lib.ptr(out),
+                                              _lib.stream_handle()))
+    o = out.cpu().numpy()
+    res = {k: o[:, i] for i, k in enumerate(("rt60", "c80", "d50", "ts", "g"))}
+    return {k: float(v[0]) for k, v in res.items()} if single else res

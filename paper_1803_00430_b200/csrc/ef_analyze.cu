@@ -61,6 +61,76 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return t;
 }
 
+struct Fit {
+    bool silent;
+    double slope, nfit;
+};
+
+// Block-cooperative Schroeder integral from the last non-zero bin
+// (truncation) and LS line over EDC in [-35,-5] dB, or
+// [-25,-5] dB when the EDC does not reach -35 dB; every thread
+// owns the contiguous chunk [lo, hi) of I(t).  DESIGN.md 3.6.
+template <class F>
+__device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_s, double* s_red,
+                             double* s_dblast) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
+    Fit out{true, 0.0, 0.0};
+    if (nnz < 3) return out;
+    const int h2 = min(hi, last + 1);
+    double csum = 0.0;
+    for (int t = h2 - 1; t >= lo; --t) csum += I(t);
+    double suf = csum;   // block inclusive suffix scan of the chunk sums
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double v = __shfl_down_sync(kAll, suf, o);
+        if (lane + o < 32) suf += v;
+    }
+    __syncthreads();
+    if (lane == 0) s_red[w] = suf;   // warp total
+    __syncthreads();
+    double after = 0.0, edc0 = 0.0;
+    for (int i = 0; i < kAWarps; ++i) {
+        if (i > w) after += s_red[i];
+        edc0 += s_red[i];
+    }
+    suf += after;
+    double acc = suf - csum;   // energy after this thread's chunk
+    for (int t = h2 - 1; t >= lo; --t) {
+        acc += I(t);
+        const double db = 10.0 * log10(acc / edc0);
+        const double x = (double)t * bin_s;
+        if (t == last) *s_dblast = db;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const double lim = r == 0 ? -35.0 : -25.0;
+            if (db <= -5.0 && db >= lim) {
+                fit[r][0] += 1.0;
+                fit[r][1] += x;
+                fit[r][2] += db;
+                fit[r][3] += x * db;
+                fit[r][4] += x * x;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int i = 0; i < 5; ++i) fit[r][i] = block_sum(fit[r][i], s_red);
+    const double db_last = *s_dblast;
+    const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
+    if (r < 0) return out;
+    const double n = fit[r][0], sx = fit[r][1], sy = fit[r][2], sxy = fit[r][3], sxx = fit[r][4];
+    const double den = n * sxx - sx * sx;
+    if (n < 2.0 || !(den > 0.0)) return out;
+    const double slope = (n * sxy - sx * sy) / den;
+    if (!(slope < 0.0)) return out;
+    out.silent = false;
+    out.slope = slope;
+    out.nfit = n;
+    return out;
+}
+
 template <int ORDER>
 __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
@@ -136,73 +206,11 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     __syncthreads();
     const double total = s_avg[0] / kY00;
 
-    // ---- pass 2: Schroeder backward integration from the last non-zero bin
-    // (truncation); LS fits on [-35,-5] and [-25,-5] dB
-    double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
-    double db_last = 0.0;
-    const bool enough = nnz >= 3;
-    if (enough) {
-        const int h2 = min(hi, last + 1);
-        double csum = 0.0;
-        for (int t = h2 - 1; t >= lo; --t) csum += (double)Hs[t * stride] / kY00;
-        // block inclusive suffix scan of the chunk sums
-        double suf = csum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double v = __shfl_down_sync(kAll, suf, o);
-            if (lane + o < 32) suf += v;
-        }
-        if (lane == 0) s_red[w] = suf;   // warp total
-        __syncthreads();
-        double after = 0.0;
-        for (int i = w + 1; i < kAWarps; ++i) after += s_red[i];
-        suf += after;
-        double edc0 = 0.0;
-        for (int i = 0; i < kAWarps; ++i) edc0 += s_red[i];
-        double acc = suf - csum;   // energy after this thread's chunk
-        for (int t = h2 - 1; t >= lo; --t) {
-            acc += (double)Hs[t * stride] / kY00;
-            const double db = 10.0 * log10(acc / edc0);
-            const double x = (double)t * P.bin_s;
-            if (t == last) s_dblast = db;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const double lim = r == 0 ? -35.0 : -25.0;
-                if (db <= -5.0 && db >= lim) {
-                    fit[r][0] += 1.0;
-                    fit[r][1] += x;
-                    fit[r][2] += db;
-                    fit[r][3] += x * db;
-                    fit[r][4] += x * x;
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int i = 0; i < 5; ++i) fit[r][i] = block_sum(fit[r][i], s_red);
-        db_last = s_dblast;
-    }
-
-    // ---- per-band outputs
-    bool silent = !enough;
-    double slope = 0.0, nfit = 0.0;
-    if (!silent) {
-        const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
-        if (r < 0) {
-            silent = true;
-        } else {
-            const double n = fit[r][0], sx = fit[r][1], sy = fit[r][2], sxy = fit[r][3], sxx = fit[r][4];
-            const double den = n * sxx - sx * sx;
-            if (n < 2.0 || !(den > 0.0)) {
-                silent = true;
-            } else {
-                slope = (n * sxy - sx * sy) / den;
-                nfit = n;
-                if (!(slope < 0.0)) silent = true;
-            }
-        }
-    }
+    // ---- pass 2: Schroeder fit (shared with the acoustic-metrics kernel)
+    const Fit fit = schroeder_fit([&](int t) { return (double)Hs[t * stride] / kY00; }, lo, hi, last,
+                                  nnz, P.bin_s, s_red, &s_dblast);
+    const bool silent = fit.silent;
+    const double slope = fit.slope, nfit = fit.nfit;
     double rt60 = 1.0;   // cold-start value for silent bands
     if (!silent) rt60 = fmin(fmax(-60.0 / slope, 0.05), P.max_rt);
     const double gain = (!silent && total > 0.0) ? sqrt(total / (rt60 / (6.0 * log(10.0)))) : 0.0;
@@ -270,6 +278,69 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     }
 }
 
+// Acoustic metrics of energy series: one CTA per series.
+__global__ void __launch_bounds__(kAThreads) metrics_kernel(const double* E, int n_bins, double bin_s,
+                                                            const int32_t* direct_index, double e_ref,
+                                                            double max_rt, double* out) {
+    __shared__ double s_red[kAWarps];
+    __shared__ double s_dblast;
+    __shared__ int s_ired[2][kAWarps];
+    const int sr = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const double* I = E + (size_t)sr * n_bins;
+    const int d0 = direct_index ? max(0, min(direct_index[sr], n_bins - 1)) : 0;
+    const int n80 = (int)llrint(0.080 / bin_s), n50 = (int)llrint(0.050 / bin_s);
+    const int chunk = (n_bins + kAThreads - 1) / kAThreads;
+    const int lo = min(tid * chunk, n_bins), hi = min(lo + chunk, n_bins);
+    int last = -1, nnz = 0;
+    double tot = 0.0, e80 = 0.0, e50 = 0.0, tsn = 0.0;
+    for (int t = lo; t < hi; ++t) {
+        const double v = I[t];
+        if (v > 0.0) {
+            last = t;
+            ++nnz;
+        }
+        if (t >= d0) {
+            tot += v;
+            if (t < d0 + n80) e80 += v;
+            if (t < d0 + n50) e50 += v;
+            tsn += ((double)(t - d0) + 0.5) * bin_s * v;   // bin centres
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        last = max(last, __shfl_xor_sync(kAll, last, o));
+        nnz += __shfl_xor_sync(kAll, nnz, o);
+    }
+    if (lane == 0) {
+        s_ired[0][w] = last;
+        s_ired[1][w] = nnz;
+    }
+    __syncthreads();
+    last = -1;
+    nnz = 0;
+    for (int i = 0; i < kAWarps; ++i) {
+        last = max(last, s_ired[0][i]);
+        nnz += s_ired[1][i];
+    }
+    tot = block_sum(tot, s_red);
+    e80 = block_sum(e80, s_red);
+    e50 = block_sum(e50, s_red);
+    tsn = block_sum(tsn, s_red);
+    if (tid == 0) s_dblast = 0.0;
+    __syncthreads();
+    const Fit fit = schroeder_fit([&](int t) { return I[t]; }, lo, hi, last, nnz, bin_s, s_red, &s_dblast);
+    if (tid == 0) {
+        double* o = out + (size_t)sr * 5;
+        o[0] = fit.silent ? -1.0 : fmin(fmax(-60.0 / fit.slope, 0.05), max_rt);
+        const double late = tot - e80;
+        o[1] = late > 0.0 ? fmin(10.0 * log10(e80 / late), 99.0) : 99.0;   // C80, +99 dB sentinel
+        o[2] = tot > 0.0 ? e50 / tot : 0.0;                                // D50
+        o[3] = tot > 0.0 ? tsn / tot : 0.0;                                // TS, s
+        o[4] = (tot > 0.0 && e_ref > 0.0) ? 10.0 * log10(tot / e_ref) : -99.0;   // G, dB
+    }
+}
+
 __global__ void blend_kernel(const float* cache, const float* frame,
                              int64_t n, float a, float b, float* out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -280,6 +351,18 @@ __global__ void blend_kernel(const float* cache, const float* frame,
 }  // namespace ef
 
 using namespace ef;
+
+extern "C" int ef_acoustic_metrics(const double* energy, int64_t n_series, int32_t n_bins,
+                                   double bin_s, const int32_t* direct_index, double e_ref,
+                                   double max_rt, double* out, void* stream) {
+    if (n_series < 0 || n_bins < 1 || !(bin_s > 0.0)) return set_error(EF_EINVAL, "ef_acoustic_metrics: bad sizes");
+    if (n_series == 0) return EF_OK;
+    if (!energy || !out) return set_error(EF_EINVAL, "ef_acoustic_metrics: null argument");
+    metrics_kernel<<<(unsigned)n_series, kAThreads, 0, (cudaStream_t)stream>>>(energy, n_bins, bin_s, direct_index,
+                                                                              e_ref, max_rt, out);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "metrics_kernel");
+}
 
 extern "C" int ef_blend(const float* cache, const float* frame, int64_t n, double alpha, float* out,
                         void* stream) {

@@ -573,3 +573,26 @@ def test_dynamic_refit_matches_rebuild_and_oracle():
     ref = _oracle_trace(_oracle_for(w2), w2, 2, np.arange(n, dtype=np.uint32))
     bad, excl = _compare_paths(tr.path_nseg.cpu().numpy()[0], tr.path_ids.cpu().numpy()[0], ref)
     assert bad == 0 and excl <= 0.01 * n
+
+
+def test_acoustic_metrics_spec_examples():
+    """SPEC.md:558-560 closed forms for an exponential decay with RT60 = 1 s:
+    C80 = 3.05 dB, D50 = 0.4988, TS = 1/(6 ln 10) = 0.0724 s; SPEC.md:563:
+    metrics invariant to scaling except G, which shifts by the scale in dB."""
+    dt = 1e-3
+    i = np.arange(3000)
+    k = 6.0 * np.log(10.0)
+    E = (10.0 ** (-6.0 * i * dt) - 10.0 ** (-6.0 * (i + 1) * dt)) / k     # exact bin integrals
+    m = analysis.acoustic_metrics(E, dt)
+    assert abs(m["c80"] - 10 * np.log10((1 - 10 ** -0.48) / 10 ** -0.48)) < 1e-6
+    assert abs(m["c80"] - 3.05) < 0.01
+    assert abs(m["d50"] - (1 - 10 ** -0.3)) < 1e-9 and abs(m["d50"] - 0.4988) < 1e-4
+    assert abs(m["ts"] - 1 / k) < 1e-4
+    assert abs(m["rt60"] - 1.0) < 0.02
+    m2 = analysis.acoustic_metrics(4.0 * E, dt)
+    for key in ("c80", "d50", "ts", "rt60"):
+        assert abs(m2[key] - m[key]) < 1e-9
+    assert abs(m2["g"] - m["g"] - 10 * np.log10(4.0)) < 1e-9
+    # direct index: the same decay starting 10 bins late gives the same metrics
+    m3 = analysis.acoustic_metrics(np.concatenate([np.zeros(10), E[:-10]]), dt, direct_index=10)
+    assert abs(m3["c80"] - m["c80"]) < 1e-6 and abs(m3["ts"] - m["ts"]) < 1e-9
