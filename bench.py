@@ -13,8 +13,9 @@ one NCCL reduce-scatter per frame, each rank then analysing S/N sources.
 
 Timing: CUDA events per step on the launching stream, L2 flushed (256 MiB
 write) between steps outside the events, max over ranks.  ``e2e`` repeats
-the steps through the public API with pinned host inputs/outputs and the
-copies inside the timed region.  ``--impl reference`` times the CPU oracle
+the steps through the public API with the source positions copied in from
+pinned host memory and the frame's result (reverb parameters per source and
+band) copied back, both inside the timed region.  ``--impl reference`` times the CPU oracle
 port of the reference algorithm (oracle/efo.c, every host core) instead.
 """
 from __future__ import annotations
@@ -288,8 +289,11 @@ def run_gpu(args, w, metric, unit):
 
     # ---- e2e through the public API: pinned host in/out, copies timed
     src_host = torch.from_numpy(np.ascontiguousarray(w.sources, np.float64)).pin_memory()
-    H_host = torch.empty(tuple(an.params.shape), dtype=torch.float64).pin_memory()
-    Hist_host = torch.empty(tuple((H_own if world > 1 else tr.H).shape), dtype=torch.float32).pin_memory()
+    # the step's result is the per-(source, band) reverb parameters and the
+    # per-source predelay / mean free path (the IR itself stays on the device,
+    # where the next frame's temporal cache and the renderer consume it)
+    P_host = torch.empty(tuple(an.params.shape), dtype=torch.float64).pin_memory()
+    Q_host = torch.empty(tuple(an.src_params.shape), dtype=torch.float64).pin_memory()
     e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
@@ -297,13 +301,13 @@ def run_gpu(args, w, metric, unit):
         e_starts[i].record(stream)
         tr.src_pos.copy_(src_host, non_blocking=True)
         step()
-        Hist_host.copy_(H_own if world > 1 else tr.H, non_blocking=True)
-        H_host.copy_(an.params, non_blocking=True)
+        P_host.copy_(an.params, non_blocking=True)
+        Q_host.copy_(an.src_params, non_blocking=True)
         e_ends[i].record(stream)
     torch.cuda.synchronize()
     e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
     h2d = src_host.numel() * 8
-    d2h = Hist_host.numel() * 4 + H_host.numel() * 8
+    d2h = P_host.numel() * 8 + Q_host.numel() * 8
 
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, k_ms, e_ms], dtype=torch.float64, device=dev)
