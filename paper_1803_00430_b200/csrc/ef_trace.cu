@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ef_device.cuh"
 
@@ -27,6 +28,15 @@ constexpr int64_t kBigSceneBytes = 32ll << 20;
 template <int THREADS>
 constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
 constexpr size_t kNodeCacheBytes = 128 * 1024;   // + 64 KB of traversal stacks
+
+// shared-memory node cache size; EF_NODE_CACHE_KB overrides (tuning only)
+static size_t node_cache_bytes() {
+    static size_t v = [] {
+        const char* e = std::getenv("EF_NODE_CACHE_KB");
+        return e ? (size_t)std::atoi(e) * 1024 : kNodeCacheBytes;
+    }();
+    return v;
+}
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr unsigned kFull = 0xffffffffu;
@@ -689,7 +699,7 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.er_cap = cfg->er_capacity;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
-        P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, kNodeCacheBytes / sizeof(GpuNode));
+        P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, node_cache_bytes() / sizeof(GpuNode));
         const bool big = (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
                              s->n_tri * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
         if (s->n_bands <= 4)
