@@ -27,7 +27,10 @@ constexpr int kBigThreads = 768;
 constexpr int64_t kBigSceneBytes = 32ll << 20;
 template <int THREADS>
 constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
-constexpr size_t kNodeCacheBytes = 128 * 1024;   // + 64 KB of traversal stacks
+// Shared-memory copy of the top of the tree: measured on B200 (C2/C3/C5) to
+// lose to leaving the space to L1 (C5 3.34 vs 2.93 G seg/s at 0 vs 128 KB,
+// C2 flat), so off by default.
+constexpr size_t kNodeCacheBytes = 0;
 
 // shared-memory node cache size; EF_NODE_CACHE_KB overrides (tuning only)
 static size_t node_cache_bytes() {
@@ -700,8 +703,13 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
         P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, node_cache_bytes() / sizeof(GpuNode));
-        const bool big = (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
-                             s->n_tri * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
+        static const int force_big = [] {
+            const char* e = std::getenv("EF_TRACE_BIG");   // tuning only: 0 / 1
+            return e ? std::atoi(e) : -1;
+        }();
+        const bool big = force_big >= 0 ? force_big == 1
+                                         : (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
+                                                   s->n_tri * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
         if (s->n_bands <= 4)
             e = dispatch<4>(brute, big, cfg->order, P, st);
         else
