@@ -20,11 +20,11 @@
 namespace ef {
 
 // One fat CTA per SM (node cache in shared memory).  Scenes whose nodes +
-// triangles exceed kBigSceneBytes (DRAM-latency-bound traversal, e.g. C5) get
+// triangles exceed kBigSceneBytes (L1 cannot hold the scene: C3, C5) get
 // 768 threads (80 registers, more warps to hide latency); smaller ones 512.
 constexpr int kSmallThreads = 512;
 constexpr int kBigThreads = 768;
-constexpr int64_t kBigSceneBytes = 32ll << 20;
+constexpr int64_t kBigSceneBytes = 4ll << 20;
 template <int THREADS>
 constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
 // Shared-memory copy of the top of the tree: measured on B200 (C2/C3/C5) to
