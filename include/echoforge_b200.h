@@ -171,7 +171,6 @@ typedef struct {
                                sphere test                  */
     int32_t er_max_order;   /* arrivals of order 1..er_max_order (<= 2) go
                                to the early-reflection list, not to H       */
-    int32_t flags;          /* bit 0: disable the cooperative tail mode    */
     int64_t er_capacity;    /* entries available at er_entries             */
     void* er_entries;       /* DEVICE ef_er_entry[er_capacity] or NULL      */
     uint32_t* er_count;     /* DEVICE counter, ACCUMULATED (caller zeroes)  */

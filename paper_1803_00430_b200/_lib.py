@@ -37,8 +37,7 @@ class TraceConfig(ctypes.Structure):
                 ("listener", ctypes.c_double * 3), ("radius", ctypes.c_double),
                 ("e0", ctypes.c_float), ("record_ids", ctypes.c_int32),
                 ("clear_outputs", ctypes.c_int32), ("diffuse_rain", ctypes.c_int32),
-                ("er_max_order", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("er_capacity", ctypes.c_int64),
+                ("er_max_order", ctypes.c_int32), ("er_capacity", ctypes.c_int64),
                 ("er_entries", ctypes.c_void_p), ("er_count", ctypes.c_void_p)]
 
 

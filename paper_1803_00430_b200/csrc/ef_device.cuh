@@ -405,102 +405,6 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, nullptr, 0, a, b);
 }
 
-// ------------------------------------------------ cooperative tail mode ----
-struct GridView {
-    const uint32_t* start;   // (n_cells + 1)
-    const uint32_t* tris;    // leaf-order triangle positions
-    int dims[3];
-    double lo[3], cell[3];
-};
-
-__device__ __forceinline__ void warp_min_hit(Hit& h) {
-    // smallest t, then lowest id among equal t (the DESIGN.md 3.2 tie rule)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double t2 = __shfl_xor_sync(0xffffffffu, h.t, o);
-        const int32_t id2 = __shfl_xor_sync(0xffffffffu, h.id, o);
-        if (t2 < h.t || (t2 == h.t && id2 < h.id)) {
-            h.t = t2;
-            h.id = id2;
-        }
-    }
-}
-
-// Closest hit answered by the whole warp for ONE ray (every lane passes the
-// same ray and gets the same result): 3-D DDA over the uniform grid, each
-// cell's triangles tested 32 at a time with the exact f64 test; the first
-// cell holding a hit with t <= its exit distance ends the walk (triangles are
-// registered in every cell their padded box overlaps, so a hit rounded past
-// the exit is found again in the next cell).  Same answers as closest_bvh.
-static __device__ __noinline__ Hit closest_grid_warp(const GridView& G, const GpuTri* __restrict__ tris,
-                                              double ox, double oy, double oz, double dx, double dy,
-                                              double dz, double t_min, double t_max, uint32_t& n_tris) {
-    const int lane = threadIdx.x & 31;
-    Hit best{t_max, INT32_MAX};
-    const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
-    double t0 = t_min, t1 = t_max;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double hi = G.lo[k] + G.cell[k] * G.dims[k];
-        if (d[k] != 0.0) {
-            const double ta = (G.lo[k] - o[k]) / d[k], tb = (hi - o[k]) / d[k];
-            t0 = fmax(t0, fmin(ta, tb));
-            t1 = fmin(t1, fmax(ta, tb));
-        } else if (o[k] < G.lo[k] || o[k] > hi) {
-            return best;
-        }
-    }
-    if (!(t0 <= t1)) return best;
-    int c[3], step[3];
-    double tnext[3], tdelta[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double p = o[k] + t0 * d[k];
-        c[k] = min(max((int)floor((p - G.lo[k]) / G.cell[k]), 0), G.dims[k] - 1);
-        if (d[k] > 0.0) {
-            step[k] = 1;
-            tnext[k] = (G.lo[k] + (c[k] + 1) * G.cell[k] - o[k]) / d[k];
-            tdelta[k] = G.cell[k] / d[k];
-        } else if (d[k] < 0.0) {
-            step[k] = -1;
-            tnext[k] = (G.lo[k] + c[k] * G.cell[k] - o[k]) / d[k];
-            tdelta[k] = -G.cell[k] / d[k];
-        } else {
-            step[k] = 0;
-            tnext[k] = INFINITY;
-            tdelta[k] = INFINITY;
-        }
-    }
-    for (;;) {
-        const double t_exit = fmin(fmin(tnext[0], tnext[1]), tnext[2]);
-        const int64_t cell = ((int64_t)c[2] * G.dims[1] + c[1]) * G.dims[0] + c[0];
-        const uint32_t a = __ldg(G.start + cell), b = __ldg(G.start + cell + 1);
-        Hit h{fmin(t_exit, t_max), INT32_MAX};
-        for (uint32_t j = a + lane; j < b; j += 32) {
-            const double2* q = reinterpret_cast<const double2*>(tris + __ldg(G.tris + j));
-            const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3),
-                          q4 = __ldg(q + 4);
-            const double v[9] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y, q4.x};
-            const int32_t id = (int32_t)__double_as_longlong(q4.y);
-            double t;
-            if (mt_hit(ox, oy, oz, dx, dy, dz, v, t_min, h.t, t) && (t < h.t || id < h.id)) {
-                h.t = t;
-                h.id = id;
-            }
-        }
-        if (lane == 0) n_tris += b - a;
-        warp_min_hit(h);
-        if (h.id != INT32_MAX) return h;
-        if (t_exit >= t1) return best;   // left the grid (or passed t_max)
-        int ax = 0;
-        if (tnext[1] < tnext[ax]) ax = 1;
-        if (tnext[2] < tnext[ax]) ax = 2;
-        c[ax] += step[ax];
-        if (c[ax] < 0 || c[ax] >= G.dims[ax]) return best;
-        tnext[ax] += tdelta[ax];
-    }
-}
-
 // ------------------------------------------------------------------ SH ----
 // Real SH, ACN order, exactly sh.py:94-125 (same expression trees).
 template <int ORDER>

@@ -50,22 +50,6 @@ struct HostBvh {
     int max_stack = 0;           // bound on traversal stack entries
 };
 
-// Uniform grid for the warp-cooperative tail mode (grid_build.cpp).
-constexpr double kGridCellsPerTri = 8.0;
-constexpr int64_t kGridMaxCells = int64_t(1) << 22;
-constexpr int64_t kGridMaxRefs = int64_t(1) << 27;
-
-struct HostGrid {
-    int32_t dims[3] = {0, 0, 0};
-    double lo[3] = {0, 0, 0};
-    double cell[3] = {0, 0, 0};
-    std::vector<uint32_t> cell_start;   // (n_cells + 1) offsets into cell_tris
-    std::vector<uint32_t> cell_tris;    // leaf-order triangle positions
-};
-
-void build_grid(const double* v0, const double* e1, const double* e2, int64_t n,
-                const std::vector<int64_t>& leaf_order, double pad, HostGrid& g);
-
 // Builds a binned-SAH BVH2 with conservative f32 boxes over the triangles
 // (v0, v0+e1, v0+e2).  Throws std::runtime_error on failure.
 void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, HostBvh& out);
@@ -95,12 +79,6 @@ struct ef_scene {
     int32_t* level_nodes = nullptr;    // node indices grouped by depth
     std::vector<int64_t> level_start;  // host copy of the level offsets
     double pad = 0.0;
-    // uniform grid of the cooperative tail mode (nullptr: none)
-    uint32_t* grid_start = nullptr;
-    uint32_t* grid_tris = nullptr;
-    int32_t grid_dims[3] = {0, 0, 0};
-    double grid_lo[3] = {0, 0, 0};
-    double grid_cell[3] = {0, 0, 0};
 };
 
 // error plumbing (ef_api.cpp)

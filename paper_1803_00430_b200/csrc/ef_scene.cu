@@ -36,8 +36,6 @@ void free_scene(ef_scene* s) {
     cudaFree(s->pdiff);
     cudaFree(s->fr);
     cudaFree(s->leaf_order);
-    cudaFree(s->grid_start);
-    cudaFree(s->grid_tris);
     cudaFree(s->level_nodes);
     delete s;
 }
@@ -134,21 +132,6 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
             EF_UP(level_nodes, bvh.level_nodes.data(), bvh.level_nodes.size());
             s->level_start = bvh.level_start;
             s->pad = bvh.pad;
-            if (n_tri > kBruteMaxTris) {   // all-pairs scenes never use the grid
-                HostGrid grid;
-                try {
-                    build_grid(v0, e1, e2, n_tri, bvh.order, bvh.pad, grid);
-                    EF_UP(grid_start, grid.cell_start.data(), grid.cell_start.size());
-                    EF_UP(grid_tris, grid.cell_tris.data(), std::max<size_t>(grid.cell_tris.size(), 1));
-                    for (int k = 0; k < 3; ++k) {
-                        s->grid_dims[k] = grid.dims[k];
-                        s->grid_lo[k] = grid.lo[k];
-                        s->grid_cell[k] = grid.cell[k];
-                    }
-                } catch (const std::exception&) {
-                    // no grid: the tail mode stays off for this scene
-                }
-            }
             EF_UP(tris, tris.data(), tris.size());
             EF_UP(tris_by_id, by_id.data(), by_id.size());
             EF_UP(normals, normals, (size_t)3 * n_tri);

@@ -42,7 +42,6 @@ static size_t node_cache_bytes() {
 }
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
-constexpr int kTailPaths = 2;   // live paths per warp at or below which the warp cooperates
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
@@ -98,7 +97,6 @@ struct TraceParams {
     unsigned int* er_count;
     int64_t er_cap;
     int32_t timing;         // debug: path_ids rows get (t0, t1, smid, nseg)
-    GridView grid;          // cooperative tail mode (grid.start == nullptr: off)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -259,37 +257,18 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             }
         }
         if (__all_sync(kFull, !active)) break;
+        if (!active) continue;
 
-        // ---- closest hit (exact f64 leaf test).  Tail mode: once the path
-        // pool is exhausted and at most kTailPaths paths are left in the
-        // warp, the whole warp answers each remaining query together (grid
-        // walk, 32 triangles per step) -- the frame's end is set by its
-        // longest paths, which otherwise run one lane at a time.
-        Hit h{INFINITY, INT32_MAX};
+        // ---- closest hit (exact f64 leaf test)
+        Hit h;
         if (BRUTE) {
-            if (!active) continue;
             h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
             ls.c[EF_ST_TRIS] += P.n_tri;
-        } else {
-            const unsigned am = __ballot_sync(kFull, active);
-            const bool tail = P.grid.start != nullptr && __popc(am) <= kTailPaths &&
-                              __any_sync(kFull, exhausted);
-            if (tail) {
-                for (unsigned m = am; m; m &= m - 1) {
-                    const int L = __ffs(m) - 1;
-                    const Hit hh = closest_grid_warp(
-                        P.grid, P.tris, __shfl_sync(kFull, ox, L), __shfl_sync(kFull, oy, L),
-                        __shfl_sync(kFull, oz, L), __shfl_sync(kFull, dx, L), __shfl_sync(kFull, dy, L),
-                        __shfl_sync(kFull, dz, L), kRayEps, INFINITY, ls.c[EF_ST_TRIS]);
-                    if (lane == L) h = hh;
-                }
-            } else if (active) {
-                h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
-                                P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
-                                s_stack + threadIdx.x, smem_stack_depth<THREADS>());
-            }
-            if (!active) continue;
         }
+        else
+            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
+                            P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
+                            s_stack + threadIdx.x, smem_stack_depth<THREADS>());
         const bool hit = h.id != INT32_MAX;
         EF_PHASE_T0(tsh);
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
@@ -716,13 +695,6 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.path_ids = (path_ids && cfg->record_ids) ? path_ids + (size_t)s0 * cfg->n_rays * cfg->max_bounces : nullptr;
         P.timing = (P.path_ids && cfg->record_ids == 2 && cfg->max_bounces >= 6) ? 1 : 0;
         P.rain = cfg->diffuse_rain ? 1 : 0;
-        P.grid.start = (cfg->flags & 1) ? nullptr : s->grid_start;   // bit 0: tail mode off
-        P.grid.tris = s->grid_tris;
-        for (int k = 0; k < 3; ++k) {
-            P.grid.dims[k] = s->grid_dims[k];
-            P.grid.lo[k] = s->grid_lo[k];
-            P.grid.cell[k] = s->grid_cell[k];
-        }
         P.fr = s->fr;
         P.er_max_order = cfg->er_entries ? std::max(0, std::min(cfg->er_max_order, 2)) : 0;
         P.er = static_cast<ef_er_entry*>(cfg->er_entries);

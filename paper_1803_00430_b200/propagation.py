@@ -40,7 +40,6 @@ class TraceConfig:
     diffuse_rain: bool = False          # next-event connection per diffuse bounce
     er_max_order: int = 0               # arrivals of order 1..er_max_order -> PathList (<= 2)
     er_capacity: int = 1 << 20          # device ER list entries per launch
-    tail_mode: bool = True              # warp-cooperative grid walk for a warp's last paths
 
     @property
     def n_coeffs(self) -> int:
@@ -226,7 +225,6 @@ class FrameTracer:
         cfg.record_ids = int(self.record)
         cfg.clear_outputs = int(bool(clear))
         cfg.diffuse_rain = int(bool(c.diffuse_rain))
-        cfg.flags = 0 if c.tail_mode else 1
         if self.er is not None:
             if clear:
                 self.er_count.zero_()
