@@ -57,7 +57,7 @@ EXPORTS = ("ef_abi_version", "ef_last_error", "ef_launch_count", "ef_scene_creat
            "ef_scene_destroy", "ef_scene_info", "ef_intersect_batch", "ef_occluded_batch",
            "ef_ray_triangles", "ef_eval_sh_batch", "ef_loudness_batch", "ef_trace", "ef_analyze", "ef_blend",
            "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process",
-           "ef_scene_refit", "ef_acoustic_metrics")
+           "ef_scene_refit", "ef_acoustic_metrics", "ef_scene_create_ex", "ef_scene_rebuild")
 
 
 def lib():
@@ -89,6 +89,9 @@ def lib():
     L.ef_blend.argtypes = [vp, vp, i64, f64, vp, vp]
     L.ef_audio_create.argtypes = [vp] * 13
     L.ef_scene_refit.argtypes = [vp] * 6
+    L.ef_scene_rebuild.argtypes = [vp] * 6
+    L.ef_scene_create_ex.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, i32, i32, ctypes.c_uint32,
+                                     ctypes.POINTER(vp)]
     L.ef_acoustic_metrics.argtypes = [vp, i64, i32, f64, vp, f64, f64, vp, vp]
     L.ef_audio_destroy.argtypes = [vp]
     L.ef_audio_info.argtypes = [vp, vp]

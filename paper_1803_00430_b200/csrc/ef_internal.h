@@ -56,6 +56,16 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
 
 }  // namespace ef
 
+struct ef_scene;
+typedef struct CUstream_st* cudaStream_t;
+namespace ef {
+// LBVH on the device (bvh_device.cu) from DEVICE triangle rows `stride`
+// doubles apart; replaces the scene's nodes, leaf order and refit schedule.
+int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const double* e2,
+                     int64_t stride, cudaStream_t st);
+
+}  // namespace ef
+
 struct ef_scene {
     int64_t n_tri = 0;
     int32_t n_bands = 0;
@@ -77,6 +87,8 @@ struct ef_scene {
     // refit support (dynamic scenes)
     int64_t* leaf_order = nullptr;     // (n_tri) leaf position -> original id
     int32_t* level_nodes = nullptr;    // node indices grouped by depth
+    int64_t n_nodes_cap = 0;           // allocated nodes (device builds over-allocate)
+    int64_t level_nodes_len = 0;
     std::vector<int64_t> level_start;  // host copy of the level offsets
     double pad = 0.0;
 };

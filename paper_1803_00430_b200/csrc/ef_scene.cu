@@ -46,7 +46,18 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
                                const double* normals, const int64_t* material_index, int64_t n_tri,
                                const double* absorption, const double* scattering,
                                int32_t n_materials, int32_t n_bands, ef_scene** out) {
+    return ef_scene_create_ex(v0, e1, e2, normals, material_index, n_tri, absorption, scattering,
+                              n_materials, n_bands, 0u, out);
+}
+
+extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const double* e2,
+                                  const double* normals, const int64_t* material_index, int64_t n_tri,
+                                  const double* absorption, const double* scattering,
+                                  int32_t n_materials, int32_t n_bands, uint32_t flags,
+                                  ef_scene** out) {
     if (!out) return set_error(EF_EINVAL, "ef_scene_create: out is null");
+    if (flags & ~(uint32_t)EF_SCENE_DEVICE_BUILD)
+        return set_error(EF_EINVAL, "ef_scene_create: unknown flags");
     *out = nullptr;
     if (n_tri < 0) return set_error(EF_EINVAL, "ef_scene_create: n_tri < 0");
     if (n_bands < 1 || n_bands > kMaxBands)
@@ -97,7 +108,32 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
         EF_UP(fs, fs.data(), fs.size());
         EF_UP(pdiff, pd.data(), pd.size());
         EF_UP(fr, fr.data(), fr.size());
-        if (n_tri > 0) {
+        if (n_tri > 0 && (flags & EF_SCENE_DEVICE_BUILD)) {
+            std::vector<double> by_id(9 * n_tri);
+            std::vector<int32_t> mat(n_tri);
+            for (int64_t t = 0; t < n_tri; ++t) {
+                for (int k = 0; k < 3; ++k) {
+                    by_id[9 * t + k] = v0[3 * t + k];
+                    by_id[9 * t + 3 + k] = e1[3 * t + k];
+                    by_id[9 * t + 6 + k] = e2[3 * t + k];
+                }
+                mat[t] = (int32_t)material_index[t];
+            }
+            EF_UP(tris_by_id, by_id.data(), by_id.size());
+            EF_UP(normals, normals, (size_t)3 * n_tri);
+            EF_UP(mat, mat.data(), mat.size());
+            if (e == cudaSuccess) e = cudaMalloc((void**)&s->tris, (size_t)n_tri * sizeof(GpuTri));
+            if (e == cudaSuccess) e = cudaMalloc((void**)&s->leaf_order, (size_t)n_tri * sizeof(int64_t));
+            if (e == cudaSuccess) {
+                s->device_bytes += n_tri * (int64_t)(sizeof(GpuTri) + sizeof(int64_t));
+                const int rc = device_build_bvh(s, s->tris_by_id, s->tris_by_id + 3,
+                                                s->tris_by_id + 6, 9, nullptr);
+                if (rc != EF_OK) {
+                    free_scene(s);
+                    return rc;
+                }
+            }
+        } else if (n_tri > 0) {
             HostBvh bvh;
             build_bvh(v0, e1, e2, n_tri, bvh);
             std::vector<GpuTri> tris(n_tri);
@@ -131,6 +167,8 @@ extern "C" int ef_scene_create(const double* v0, const double* e1, const double*
             EF_UP(leaf_order, bvh.order.data(), bvh.order.size());
             EF_UP(level_nodes, bvh.level_nodes.data(), bvh.level_nodes.size());
             s->level_start = bvh.level_start;
+            s->n_nodes_cap = s->n_nodes;
+            s->level_nodes_len = (int64_t)bvh.level_nodes.size();
             s->pad = bvh.pad;
             EF_UP(tris, tris.data(), tris.size());
             EF_UP(tris_by_id, by_id.data(), by_id.size());
@@ -196,6 +234,20 @@ __global__ void update_tris_kernel(ef::GpuTri* tris, double* by_id, double* norm
     }
 }
 
+__global__ void copy_rows_kernel(double* by_id, double* normals_out, const double* v0,
+                                 const double* e1, const double* e2, const double* normals,
+                                 int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        for (int k = 0; k < 3; ++k) {
+            by_id[9 * i + k] = v0[3 * i + k];
+            by_id[9 * i + 3 + k] = e1[3 * i + k];
+            by_id[9 * i + 6 + k] = e2[3 * i + k];
+            normals_out[3 * i + k] = normals[3 * i + k];
+        }
+    }
+}
+
 __global__ void refit_level_kernel(ef::GpuNode* nodes, const ef::GpuTri* tris,
                                    const int32_t* level, int64_t count, double pad) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -237,6 +289,21 @@ __global__ void refit_level_kernel(ef::GpuNode* nodes, const ef::GpuTri* tris,
 }
 
 }  // namespace
+
+extern "C" int ef_scene_rebuild(ef_scene* s, const double* v0, const double* e1, const double* e2,
+                                const double* normals, void* stream) {
+    if (!s || !v0 || !e1 || !e2 || !normals) return set_error(EF_EINVAL, "ef_scene_rebuild: null argument");
+    if (s->n_tri == 0) return EF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = s->n_tri;
+    // original-order copies first (the all-pairs path and the shading normals)
+    copy_rows_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(
+        s->tris_by_id, s->normals, v0, e1, e2, normals, n);
+    count_launch();
+    const int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
+    if (rc != EF_OK) return rc;
+    return device_build_bvh(s, v0, e1, e2, 3, st);
+}
 
 extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, const double* e2,
                               const double* normals, void* stream) {
