@@ -182,7 +182,9 @@ def config_block(args, w, world):
             "triangles": int(w.n_tri), "sources": int(len(w.sources)),
             "rays_per_source_per_rank": int(w.n_rays), "max_bounces": int(w.max_bounces),
             "sh_order": int(w.order), "bands": int(w.n_bands), "bins": int(w.n_bins),
-            "parallelism": f"rays sharded x{world}, NCCL reduce-scatter of histograms" if world > 1
+            "parallelism": (f"rays sharded x{world}, " + (
+                "histograms reduce-scattered inside the trace kernel (ef_trace_fused, peer memory)"
+                if args.exchange == "fused" else "NCCL reduce-scatter of histograms")) if world > 1
             else "single GPU", "l2": "flushed between steps (256 MiB write)"}
 
 
@@ -197,9 +199,13 @@ def run_gpu(args, w, metric, unit):
     from paper_1803_00430_b200.scene import scene_from_workload
 
     world, rank, local = dist_env()
+    local = local % torch.cuda.device_count()   # gloo plumbing runs may share one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:   # plumbing checks with several ranks on one GPU (fused exchange only)
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     sc = scene_from_workload(w)
     S = len(w.sources)
@@ -212,7 +218,13 @@ def run_gpu(args, w, metric, unit):
     S_own = S // world
     an = Analyzer(S_own, w.n_bins, sc.n_bands, w.order, w.bin_s)
     nk = cfg.n_coeffs
-    if world > 1:
+    fused = world > 1 and args.exchange == "fused"
+    if fused:
+        from paper_1803_00430_b200.distributed import PeerHistograms
+        peers = PeerHistograms(S, w.n_bins, sc.n_bands, cfg.n_coeffs)
+        st_all = torch.empty_like(tr.stats)
+        su_all = torch.empty_like(tr.sum_t)
+    elif world > 1:
         H_own = torch.empty((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
         D_own = torch.empty((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
         st_own = torch.empty((S_own, tr.stats.shape[1]), dtype=torch.int64, device=dev)
@@ -230,8 +242,8 @@ def run_gpu(args, w, metric, unit):
         pos_all = torch.tensor(np.stack([w.source_positions(f) for f in range(w.n_frames)]),
                                dtype=torch.float64, device=dev)
         alpha = 1.0 - float(np.exp(-w.frame_dt / TAU_LR))
-        H_cache = torch.zeros_like(H_own if world > 1 else tr.H)
-        D_cache = torch.zeros_like(D_own if world > 1 else tr.Dir)
+        H_cache = torch.zeros((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
+        D_cache = torch.zeros((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
     seg_total = torch.zeros((), dtype=torch.int64, device=dev)
     counter = [0]
 
@@ -240,12 +252,28 @@ def run_gpu(args, w, metric, unit):
         counter[0] += 1
         if dynamic:
             tr.src_pos.copy_(pos_all[f])
+        seq = counter[0]
         if kernel_events:
             kernel_events[0].record(stream)
-        tr.trace(w.listener, frame=f, ray0=ray0, total_rays=total_rays)
+        if fused:
+            peers.begin_frame(seq)
+            tr.trace_fused(w.listener, peers, frame=f, ray0=ray0, total_rays=total_rays, slot=seq)
+        else:
+            tr.trace(w.listener, frame=f, ray0=ray0, total_rays=total_rays)
         if kernel_events:
             kernel_events[1].record(stream)
-        if world > 1:
+        if fused:
+            # the histograms are complete once every rank's trace finished;
+            # the 88-byte-per-source counters take one small all-reduce
+            st_all.copy_(tr.stats)
+            su_all.copy_(tr.sum_t)
+            dist.all_reduce(st_all)
+            dist.all_reduce(su_all)
+            peers.end_frame()
+            hs, ds = peers.block(seq)
+            own = slice(rank * S_own, (rank + 1) * S_own)
+            sts, sus = st_all[own], su_all[own]
+        elif world > 1:
             dist.reduce_scatter_tensor(H_own, tr.H)
             dist.reduce_scatter_tensor(D_own, tr.Dir)
             dist.reduce_scatter_tensor(st_own, tr.stats)
@@ -331,6 +359,8 @@ def run_gpu(args, w, metric, unit):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     if world > 1:
+        if fused:
+            peers.close()
         dist.barrier()
         dist.destroy_process_group()   # every rank tears NCCL down before exit
     if rank != 0:
@@ -500,6 +530,11 @@ def main():
     ap.add_argument("--cpu-fraction", type=float, default=None,
                     help="fraction of each source's rays in the CPU sample (default per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: histogram reduce-scatter inside the trace kernel over peer "
+                         "memory (fused) or a separate NCCL reduce-scatter")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: several ranks on one GPU for plumbing checks (fused only)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum wall time of the CPU baseline sample")
     args = ap.parse_args()

@@ -216,6 +216,33 @@ int ef_trace(const ef_scene* scene, const ef_trace_config* cfg, const double* sr
              unsigned long long* stats, double* sum_t, int32_t* path_nseg, int32_t* path_ids,
              void* stream);
 
+/* ---- multi-GPU: trace fused with the histogram reduce-scatter ---------
+ * One process per GPU, rays sharded by global index (ray0).  Instead of a
+ * local (n_sources, ...) histogram followed by a reduce-scatter, every splat
+ * of global source g is added straight into the block g % sources_per_rank
+ * of rank g / sources_per_rank through DEVICE pointer tables (one entry per
+ * rank): hist_peers[r] -> (sources_per_rank, n_bins, n_bands, nk) f32,
+ * dir_peers[r] -> (sources_per_rank, n_bands, nk) f32, mapped with
+ * ef_peer_open (remote atomics over NVLink/NVSwitch).  The blocks are
+ * ACCUMULATED and owned by their rank: clear_outputs clears only the local
+ * stats / sum_t, and the caller orders "owner zeroed" before and "all ranks
+ * done" after the launch (distributed.PeerHistograms double-buffers so one
+ * barrier per frame suffices).  Replaces bench.py's ef_trace +
+ * reduce_scatter_tensor pair. */
+int ef_trace_fused(const ef_scene* scene, const ef_trace_config* cfg, const double* src_pos,
+                   const uint32_t* src_key, const uint32_t* ray_ids, float* const* hist_peers,
+                   float* const* dir_peers, int32_t sources_per_rank, unsigned long long* stats,
+                   double* sum_t, int32_t* path_nseg, int32_t* path_ids, void* stream);
+
+#define EF_IPC_HANDLE_BYTES 64
+/* cudaMalloc'd, zeroed device buffer of `bytes` and its IPC handle
+ * (EF_IPC_HANDLE_BYTES bytes written to ipc_handle). */
+int ef_peer_alloc(int64_t bytes, void** dev_ptr, void* ipc_handle);
+int ef_peer_free(void* dev_ptr);
+/* Map another process's ef_peer_alloc buffer (same node). */
+int ef_peer_open(const void* ipc_handle, void** dev_ptr);
+int ef_peer_close(void* dev_ptr);
+
 /* ---- ir-analysis ------------------------------------------------------
  * Replaces estimate_rt60, reverb_gain (290),
  * estimate_predelay (299), average_directivity (308) and

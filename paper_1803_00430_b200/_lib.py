@@ -57,7 +57,8 @@ EXPORTS = ("ef_abi_version", "ef_last_error", "ef_launch_count", "ef_scene_creat
            "ef_scene_destroy", "ef_scene_info", "ef_intersect_batch", "ef_occluded_batch",
            "ef_ray_triangles", "ef_eval_sh_batch", "ef_loudness_batch", "ef_trace", "ef_analyze", "ef_blend",
            "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process",
-           "ef_scene_refit", "ef_acoustic_metrics", "ef_scene_create_ex", "ef_scene_rebuild")
+           "ef_scene_refit", "ef_acoustic_metrics", "ef_scene_create_ex", "ef_scene_rebuild",
+           "ef_trace_fused", "ef_peer_alloc", "ef_peer_free", "ef_peer_open", "ef_peer_close")
 
 
 def lib():
@@ -90,6 +91,12 @@ def lib():
     L.ef_audio_create.argtypes = [vp] * 13
     L.ef_scene_refit.argtypes = [vp] * 6
     L.ef_scene_rebuild.argtypes = [vp] * 6
+    L.ef_trace_fused.argtypes = [vp, ctypes.POINTER(TraceConfig), vp, vp, vp, vp, vp, i32, vp, vp,
+                                 vp, vp, vp]
+    L.ef_peer_alloc.argtypes = [i64, ctypes.POINTER(vp), vp]
+    L.ef_peer_free.argtypes = [vp]
+    L.ef_peer_open.argtypes = [vp, ctypes.POINTER(vp)]
+    L.ef_peer_close.argtypes = [vp]
     L.ef_scene_create_ex.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, i32, i32, ctypes.c_uint32,
                                      ctypes.POINTER(vp)]
     L.ef_acoustic_metrics.argtypes = [vp, i64, i32, f64, vp, f64, f64, vp, vp]
@@ -156,6 +163,20 @@ def to_device(x, dtype, shape=None):
     if shape is not None:
         y = y.reshape(shape)
     return y.contiguous()
+
+
+class DeviceArray:
+    """A raw device pointer as a torch-importable array (CUDA array
+    interface); keeps `owner` alive."""
+
+    def __init__(self, address: int, shape, typestr: str = "<f4", owner=None):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(address), False), "version": 3,
+                                         "strides": None}
+
+    def tensor(self):
+        return torch().as_tensor(self, device=device())
 
 
 def host_ptr(a: np.ndarray):

@@ -83,6 +83,12 @@ struct TraceParams {
     float e0;
     float* H;
     float* Dir;
+    // fused multi-GPU accumulation (ef_trace_fused): histogram / direct blocks
+    // of global source g live on rank g / spr at block g % spr; null = H/Dir
+    float* const* Hp;
+    float* const* Dp;
+    int32_t spr;
+    int32_t src0;           // global index of this launch's source 0
     unsigned long long* stats;
     double* sum_t;
     int32_t* path_nseg;
@@ -124,6 +130,17 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats
     ls.sum_t = 0.0;
 }
 
+// Block of launch source `src` in the peer table: rank g / spr, block g % spr
+// (its histogram or direct-sound block is `per` floats).  Remote atomics go
+// over NVLink to the owning GPU, so the frame's reduce-scatter happens inside
+// the trace kernel, splat by splat.
+__device__ __forceinline__ float* peer_block(float* const* tab, const TraceParams& P, int src,
+                                             size_t per) {
+    const int g = P.src0 + src;
+    const int o = g / P.spr;
+    return tab[o] + (size_t)(g - o * P.spr) * per;
+}
+
 // One listener arrival of order `order` (reflections before it) at path
 // length `dist` from arrival direction (ux,uy,uz) with per-band energies c[]:
 // order 0 -> Dir, 1..er_max_order -> early-reflection list (when enabled),
@@ -138,7 +155,7 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
     float* dst = nullptr;
     if (order == 0) {
         ls.c[EF_ST_DIRECT]++;
-        dst = P.Dir + (size_t)src * nb * NK;
+        dst = P.Dp ? peer_block(P.Dp, P, src, (size_t)nb * NK) : P.Dir + (size_t)src * nb * NK;
     } else if (order <= P.er_max_order) {
         const unsigned int slot = atomicAdd(P.er_count, 1u);
         if (slot < (unsigned int)P.er_cap) {
@@ -158,7 +175,8 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
     } else {
         const double q = dist / P.bin_len;
         if (q < (double)P.n_bins)
-            dst = P.H + ((size_t)src * P.n_bins + (size_t)q) * nb * NK;
+            dst = (P.Hp ? peer_block(P.Hp, P, src, (size_t)P.n_bins * nb * NK)
+                        : P.H + (size_t)src * P.n_bins * nb * NK) + (size_t)q * nb * NK;
         else
             ls.c[EF_ST_DROPPED]++;
     }
@@ -622,10 +640,14 @@ extern "C" int ef_eval_sh_batch(const double* dirs, int64_t n, int32_t order, do
     return check_cuda(cudaGetLastError(), "eval_sh_kernel");
 }
 
-extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
-                        const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
-                        unsigned long long* stats, double* sum_t, int32_t* path_nseg,
-                        int32_t* path_ids, void* stream) {
+namespace {
+
+// ef_trace and ef_trace_fused: either local H/Dir, or the peer tables Hp/Dp
+// with `spr` sources per rank (H = Dir = null).
+int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
+               const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
+               float* const* Hp, float* const* Dp, int32_t spr, unsigned long long* stats,
+               double* sum_t, int32_t* path_nseg, int32_t* path_ids, void* stream) {
     if (!s || !cfg) return set_error(EF_EINVAL, "ef_trace: null scene or config");
     if (cfg->n_sources < 1) return set_error(EF_EINVAL, "ef_trace: need at least one source");
     if (cfg->order < 0 || cfg->order > kMaxOrder) return set_error(EF_EINVAL, "ef_trace: order must be in [0, 4]");
@@ -637,7 +659,11 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
     if (cfg->mode < 0 || cfg->mode > 2) return set_error(EF_EINVAL, "ef_trace: mode must be 0, 1 or 2");
     if (cfg->er_entries && (!cfg->er_count || cfg->er_capacity < 0))
         return set_error(EF_EINVAL, "ef_trace: an early-reflection list needs er_count and er_capacity >= 0");
-    if (!src_pos || !H || !Dir || !stats || !sum_t) return set_error(EF_EINVAL, "ef_trace: null buffer");
+    const bool fused = Hp != nullptr;
+    if (!src_pos || !stats || !sum_t || (fused ? !Dp : (!H || !Dir)))
+        return set_error(EF_EINVAL, "ef_trace: null buffer");
+    if (fused && (spr < 1 || cfg->n_sources % spr != 0))
+        return set_error(EF_EINVAL, "ef_trace_fused: sources_per_rank must divide n_sources");
     if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_trace: empty scene is handled by the host");
     const bool brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= kBruteMaxTris);
     if (brute && s->n_tri > 2048) return set_error(EF_EINVAL, "ef_trace: all-pairs mode supports <= 2048 triangles");
@@ -646,9 +672,12 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
     cudaError_t e = cudaSuccess;
     if (cfg->clear_outputs) {
         // DMA-engine clears, no kernel launch
+        // (fused: the peer blocks belong to their owners, only local outputs)
         const size_t nh = (size_t)cfg->n_sources * cfg->n_bins * s->n_bands * nk;
-        e = cudaMemsetAsync(H, 0, nh * sizeof(float), st);
-        if (e == cudaSuccess) e = cudaMemsetAsync(Dir, 0, (size_t)cfg->n_sources * s->n_bands * nk * sizeof(float), st);
+        if (!fused) {
+            e = cudaMemsetAsync(H, 0, nh * sizeof(float), st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(Dir, 0, (size_t)cfg->n_sources * s->n_bands * nk * sizeof(float), st);
+        }
         if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, (size_t)cfg->n_sources * EF_ST_COUNT * 8, st);
         if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
         if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
@@ -687,8 +716,12 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
         P.lz = cfg->listener[2];
         P.r2 = cfg->radius * cfg->radius;
         P.e0 = cfg->e0;
-        P.H = H + (size_t)s0 * cfg->n_bins * s->n_bands * nk;
-        P.Dir = Dir + (size_t)s0 * s->n_bands * nk;
+        P.H = fused ? nullptr : H + (size_t)s0 * cfg->n_bins * s->n_bands * nk;
+        P.Dir = fused ? nullptr : Dir + (size_t)s0 * s->n_bands * nk;
+        P.Hp = Hp;
+        P.Dp = fused ? Dp : nullptr;
+        P.spr = fused ? spr : 1;
+        P.src0 = s0;
         P.stats = stats + (size_t)s0 * EF_ST_COUNT;
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
@@ -719,6 +752,26 @@ extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const dou
     cudaError_t e2 = cudaFreeAsync(counter, st);
     if (e != cudaSuccess) return check_cuda(e, "trace_kernel");
     return check_cuda(e2, "cudaFreeAsync");
+}
+
+}  // namespace
+
+extern "C" int ef_trace(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
+                        const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
+                        unsigned long long* stats, double* sum_t, int32_t* path_nseg,
+                        int32_t* path_ids, void* stream) {
+    return trace_impl(s, cfg, src_pos, src_key, ray_ids, H, Dir, nullptr, nullptr, 1, stats, sum_t,
+                      path_nseg, path_ids, stream);
+}
+
+extern "C" int ef_trace_fused(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
+                              const uint32_t* src_key, const uint32_t* ray_ids,
+                              float* const* hist_peers, float* const* dir_peers,
+                              int32_t sources_per_rank, unsigned long long* stats, double* sum_t,
+                              int32_t* path_nseg, int32_t* path_ids, void* stream) {
+    if (!hist_peers || !dir_peers) return set_error(EF_EINVAL, "ef_trace_fused: null peer table");
+    return trace_impl(s, cfg, src_pos, src_key, ray_ids, nullptr, nullptr, hist_peers, dir_peers,
+                      sources_per_rank, stats, sum_t, path_nseg, path_ids, stream);
 }
 
 extern "C" int ef_ray_triangles(const double* origins, const double* dirs, int64_t n_rays,

@@ -39,3 +39,175 @@ def reduce_scatter_sources(full, group=None):
     buf = full.clone()
     dist.all_reduce(buf, group=group)
     return buf[sl].contiguous()
+
+
+# --------------------------------------------------------------------------
+# Fused trace + reduce-scatter over peer memory (ef_trace_fused)
+
+class _CudaPeerBackend:
+    """Device buffers through the C ABI: cudaMalloc + CUDA IPC handles."""
+
+    def alloc(self, nbytes: int):
+        import ctypes
+
+        from . import _lib
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib().ef_peer_alloc(int(nbytes), ctypes.byref(p), h))
+        return p.value, h.raw
+
+    def open(self, handle: bytes):
+        import ctypes
+
+        from . import _lib
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib().ef_peer_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(p)))
+        return p.value
+
+    def close(self, ptr):
+        from . import _lib
+        _lib.lib().ef_peer_close(ptr)
+
+    def free(self, ptr):
+        from . import _lib
+        _lib.lib().ef_peer_free(ptr)
+
+    def table(self, ptrs):
+        from . import _lib
+        t = _lib.torch()
+        return t.tensor([int(p) for p in ptrs], dtype=t.int64, device=_lib.device())
+
+    def view(self, ptr, shape):
+        from . import _lib
+        return _lib.DeviceArray(ptr, shape).tensor()
+
+    def sync(self):
+        from . import _lib
+        _lib.torch().cuda.current_stream().synchronize()
+
+
+class PeerHistograms:
+    """This rank's share of the frame histograms, in peer-mapped memory.
+
+    Rank r owns sources [r*S/N, (r+1)*S/N) (owned_sources).  Its histogram
+    and direct-sound blocks are allocated here (ef_peer_alloc), the CUDA IPC
+    handles are exchanged once (all_gather_object), and every rank maps every
+    other rank's blocks (ef_peer_open) into two pointer tables.  The trace
+    kernels of all ranks (FrameTracer.trace_fused -> ef_trace_fused) then add
+    each splat straight into the owner's block over NVLink/NVSwitch: the
+    reduce-scatter happens inside the trace, with no NCCL call after it.
+
+    Double-buffered so that one barrier per frame orders everything: frame f
+    accumulates into parity f & 1; ``begin_frame(f)`` zeroes this rank's
+    parity (f+1) & 1 blocks for the next frame (after the owner consumed them
+    two frames ago, stream order); ``end_frame()`` synchronises the stream and
+    barriers, after which ``block(f)`` holds the complete sums of this rank's
+    sources.  Both parities start zeroed."""
+
+    def __init__(self, n_sources: int, n_bins: int, n_bands: int, nk: int, group=None,
+                 backend=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        owned_sources(n_sources, self.rank, self.world)          # validates S % N == 0
+        spr = n_sources // self.world
+        self.sources_per_rank = spr
+        self.shape_h = (spr, n_bins, n_bands, nk)
+        self.shape_d = (spr, n_bands, nk)
+        be = backend if backend is not None else _CudaPeerBackend()
+        self._be = be
+        nh = 4 * spr * n_bins * n_bands * nk
+        nd = 4 * spr * n_bands * nk
+        self._own = [(be.alloc(nh), be.alloc(nd)) for _ in range(2)]   # [(ptr, handle)] per parity
+        mine = [(h[1], d[1]) for h, d in self._own]
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self._tab = []
+        for parity in range(2):
+            hp, dp = [], []
+            for r in range(self.world):
+                if r == self.rank:
+                    hp.append(self._own[parity][0][0])
+                    dp.append(self._own[parity][1][0])
+                else:
+                    ph = be.open(allh[r][parity][0])
+                    pd = be.open(allh[r][parity][1])
+                    self._opened += [ph, pd]
+                    hp.append(ph)
+                    dp.append(pd)
+            self._tab.append((be.table(hp), be.table(dp)))
+        self._H = [be.view(self._own[p][0][0], self.shape_h) for p in range(2)]
+        self._D = [be.view(self._own[p][1][0], self.shape_d) for p in range(2)]
+
+    def tables(self, frame: int):
+        """(hist table, dir table) device pointer arrays for frame's parity."""
+        return self._tab[frame & 1]
+
+    def block(self, frame: int):
+        """(H, Dir) of this rank's sources for `frame` (complete after end_frame)."""
+        return self._H[frame & 1], self._D[frame & 1]
+
+    def begin_frame(self, frame: int):
+        nxt = (frame + 1) & 1
+        self._H[nxt].zero_()
+        self._D[nxt].zero_()
+
+    def end_frame(self):
+        import torch.distributed as dist
+
+        self._be.sync()
+        dist.barrier(group=self.group)
+
+    def close(self):
+        import torch.distributed as dist
+
+        if self._own is None:
+            return
+        self._be.sync()
+        dist.barrier(group=self.group)        # no peer still writes into our blocks
+        for p in self._opened:
+            self._be.close(p)
+        for (ph, _), (pd, _) in self._own:
+            self._be.free(ph)
+            self._be.free(pd)
+        self._own = None
+        self._opened = []
+
+
+class EmulatedPeers:
+    """N virtual ranks in one process and one GPU: every rank's blocks are
+    local tensors and the pointer tables point at them, so ef_trace_fused
+    runs exactly the addressing of the multi-GPU path (tests, 1-GPU boxes)."""
+
+    def __init__(self, n_ranks: int, n_sources: int, n_bins: int, n_bands: int, nk: int):
+        from . import _lib
+        t = _lib.torch()
+        dev = _lib.device()
+        owned_sources(n_sources, 0, n_ranks)
+        spr = n_sources // n_ranks
+        self.world = n_ranks
+        self.sources_per_rank = spr
+        self._H = [[t.zeros((spr, n_bins, n_bands, nk), dtype=t.float32, device=dev)
+                    for _ in range(n_ranks)] for _ in range(2)]
+        self._D = [[t.zeros((spr, n_bands, nk), dtype=t.float32, device=dev)
+                    for _ in range(n_ranks)] for _ in range(2)]
+        self._tab = [(t.tensor([x.data_ptr() for x in self._H[p]], dtype=t.int64, device=dev),
+                      t.tensor([x.data_ptr() for x in self._D[p]], dtype=t.int64, device=dev))
+                     for p in range(2)]
+
+    def tables(self, frame: int):
+        return self._tab[frame & 1]
+
+    def block(self, frame: int, rank: int):
+        return self._H[frame & 1][rank], self._D[frame & 1][rank]
+
+    def begin_frame(self, frame: int):
+        nxt = (frame + 1) & 1
+        for x in self._H[nxt] + self._D[nxt]:
+            x.zero_()
+
+    def end_frame(self):
+        pass

@@ -196,10 +196,7 @@ class FrameTracer:
         self.stats.zero_()
         self.sum_t.zero_()
 
-    def trace(self, listener, frame: int = 0, ray0: int = 0, n_rays: int | None = None,
-              total_rays: int | None = None, ray_ids=None, clear: bool = True, stream=None):
-        """Launch ef_trace for all sources (rays [ray0, ray0+n_rays) of each,
-        or the explicit global indices ``ray_ids``)."""
+    def _launch_config(self, listener, frame, ray0, n_rays, total_rays, ray_ids, clear):
         t = _lib.torch()
         c = self.config
         ids = None
@@ -237,10 +234,32 @@ class FrameTracer:
             self.path_nseg = t.zeros((self.n_sources, n_rays), dtype=t.int32, device=self.H.device)
             self.path_ids = t.full((self.n_sources, n_rays, c.max_order), -2, dtype=t.int32,
                                    device=self.H.device)
+        return cfg, ids
+
+    def trace(self, listener, frame: int = 0, ray0: int = 0, n_rays: int | None = None,
+              total_rays: int | None = None, ray_ids=None, clear: bool = True, stream=None):
+        """Launch ef_trace for all sources (rays [ray0, ray0+n_rays) of each,
+        or the explicit global indices ``ray_ids``)."""
+        cfg, ids = self._launch_config(listener, frame, ray0, n_rays, total_rays, ray_ids, clear)
         _lib.check(_lib.lib().ef_trace(
             self._handle, cfg, _lib.ptr(self.src_pos), _lib.ptr(self.src_key), _lib.ptr(ids),
             _lib.ptr(self.H), _lib.ptr(self.Dir), _lib.ptr(self.stats), _lib.ptr(self.sum_t),
             _lib.ptr(self.path_nseg), _lib.ptr(self.path_ids), _lib.stream_handle(stream)))
+
+    def trace_fused(self, listener, peers, frame: int = 0, ray0: int = 0, n_rays: int | None = None,
+                    total_rays: int | None = None, ray_ids=None, stream=None, slot: int | None = None):
+        """Multi-GPU frame slice through ef_trace_fused: the splats of every
+        source go straight into its owner's block of ``peers``
+        (distributed.PeerHistograms, buffer ``slot`` -- the frame sequence
+        number given to begin_frame, default ``frame``), so no reduce-scatter
+        follows.  Stats / sum_t / ER stay local to this tracer."""
+        cfg, ids = self._launch_config(listener, frame, ray0, n_rays, total_rays, ray_ids, True)
+        tab_h, tab_d = peers.tables(frame if slot is None else slot)
+        _lib.check(_lib.lib().ef_trace_fused(
+            self._handle, cfg, _lib.ptr(self.src_pos), _lib.ptr(self.src_key), _lib.ptr(ids),
+            _lib.ptr(tab_h), _lib.ptr(tab_d), peers.sources_per_rank, _lib.ptr(self.stats),
+            _lib.ptr(self.sum_t), _lib.ptr(self.path_nseg), _lib.ptr(self.path_ids),
+            _lib.stream_handle(stream)))
 
     def early_reflections(self) -> np.ndarray:
         """Raw ER arrivals of the last trace (structured ef_er_entry array)."""
