@@ -118,8 +118,10 @@ int ef_scene_refit(ef_scene* scene, const double* v0, const double* e1, const do
 int ef_scene_rebuild(ef_scene* scene, const double* v0, const double* e1, const double* e2,
                      const double* normals, void* stream);
 /* out[0]=n_tri out[1]=n_nodes out[2]=max_depth out[3]=device bytes
- * out[4]=max leaf size out[5]=n_bands out[6]=n_materials */
-int ef_scene_info(const ef_scene* scene, int64_t* out7);
+ * out[4]=max leaf size out[5]=n_bands out[6]=n_materials
+ * out[7]=triangle references in the leaves (> n_tri where spatial splits
+ * share a triangle between leaves) */
+int ef_scene_info(const ef_scene* scene, int64_t* out8);
 
 /* ---- ray queries ------------------------------------------------------
  * Replaces SceneModel.intersect_batch (scene.py:208-230), BVH.intersect

@@ -481,6 +481,7 @@ int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const doub
         s->device_bytes += n_nodes * (int64_t)sizeof(int32_t);
     }
     s->n_nodes = n_nodes;
+    s->n_refs = n64;
     s->max_depth = levels;
     s->max_leaf = h_bb.max_leaf;
     double scale;

@@ -44,7 +44,8 @@ struct HostBvh {
     std::vector<int32_t> level_nodes;   // node indices grouped by depth (root level first)
     std::vector<int64_t> level_start;   // offsets into level_nodes, size levels + 1
     double pad = 0.0;                   // absolute box padding used by the build
-    std::vector<int64_t> order;  // leaf-order position -> original triangle id
+    std::vector<int64_t> order;  // leaf-order position -> original triangle id (repeats
+                                 // where spatial splits share a triangle between leaves)
     int max_depth = 0;           // of the 4-wide tree
     int max_leaf = 0;
     int max_stack = 0;           // bound on traversal stack entries
@@ -68,6 +69,7 @@ int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const doub
 
 struct ef_scene {
     int64_t n_tri = 0;
+    int64_t n_refs = 0;                // triangle references in leaf order (>= n_tri with spatial splits)
     int32_t n_bands = 0;
     int32_t n_mat = 0;
     int64_t n_nodes = 0;
@@ -76,7 +78,7 @@ struct ef_scene {
     int64_t device_bytes = 0;
     // device buffers
     ef::GpuNode* nodes = nullptr;      // (n_nodes)
-    ef::GpuTri* tris = nullptr;        // (n_tri) leaf order
+    ef::GpuTri* tris = nullptr;        // (n_refs) leaf order
     double* tris_by_id = nullptr;      // (n_tri, 9) original order (all-pairs path)
     double* normals = nullptr;         // (n_tri, 3) original order
     int32_t* mat = nullptr;            // (n_tri)
@@ -85,7 +87,7 @@ struct ef_scene {
     double* pdiff = nullptr;           // (n_mat) probability of a diffuse bounce
     float* fr = nullptr;               // (n_mat, n_bands) (1 - a) * s for diffuse rain
     // refit support (dynamic scenes)
-    int64_t* leaf_order = nullptr;     // (n_tri) leaf position -> original id
+    int64_t* leaf_order = nullptr;     // (n_refs) leaf position -> original id
     int32_t* level_nodes = nullptr;    // node indices grouped by depth
     int64_t n_nodes_cap = 0;           // allocated nodes (device builds over-allocate)
     int64_t level_nodes_len = 0;

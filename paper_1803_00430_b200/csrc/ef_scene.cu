@@ -122,6 +122,7 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
             EF_UP(tris_by_id, by_id.data(), by_id.size());
             EF_UP(normals, normals, (size_t)3 * n_tri);
             EF_UP(mat, mat.data(), mat.size());
+            s->n_refs = n_tri;
             if (e == cudaSuccess) e = cudaMalloc((void**)&s->tris, (size_t)n_tri * sizeof(GpuTri));
             if (e == cudaSuccess) e = cudaMalloc((void**)&s->leaf_order, (size_t)n_tri * sizeof(int64_t));
             if (e == cudaSuccess) {
@@ -136,10 +137,11 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
         } else if (n_tri > 0) {
             HostBvh bvh;
             build_bvh(v0, e1, e2, n_tri, bvh);
-            std::vector<GpuTri> tris(n_tri);
+            const int64_t n_refs = (int64_t)bvh.order.size();
+            std::vector<GpuTri> tris(n_refs);
             std::vector<double> by_id(9 * n_tri);
             std::vector<int32_t> mat(n_tri);
-            for (int64_t i = 0; i < n_tri; ++i) {
+            for (int64_t i = 0; i < n_refs; ++i) {
                 const int64_t id = bvh.order[i];
                 for (int k = 0; k < 3; ++k) {
                     tris[i].v[k] = v0[3 * id + k];
@@ -156,6 +158,7 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
                 }
                 mat[t] = (int32_t)material_index[t];
             }
+            s->n_refs = n_refs;
             s->n_nodes = (int64_t)bvh.nodes.size();
             s->max_depth = bvh.max_depth;
             s->max_leaf = bvh.max_leaf;
@@ -196,6 +199,7 @@ extern "C" int ef_scene_destroy(ef_scene* s) {
 extern "C" int ef_scene_info(const ef_scene* s, int64_t* o) {
     if (!s || !o) return set_error(EF_EINVAL, "ef_scene_info: null argument");
     o[0] = s->n_tri;
+    o[7] = s->n_refs;
     o[1] = s->n_nodes;
     o[2] = s->max_depth;
     o[3] = s->device_bytes;
@@ -213,18 +217,22 @@ namespace {
 
 __global__ void update_tris_kernel(ef::GpuTri* tris, double* by_id, double* normals_out,
                                    const int64_t* order, const double* v0, const double* e1,
-                                   const double* e2, const double* normals, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+                                   const double* e2, const double* normals, int64_t n,
+                                   int64_t n_refs) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_refs || i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t id = order[i];
-        ef::GpuTri t;
-        for (int k = 0; k < 3; ++k) {
-            t.v[k] = v0[3 * id + k];
-            t.v[3 + k] = e1[3 * id + k];
-            t.v[6 + k] = e2[3 * id + k];
+        if (i < n_refs) {
+            const int64_t id = order[i];
+            ef::GpuTri t;
+            for (int k = 0; k < 3; ++k) {
+                t.v[k] = v0[3 * id + k];
+                t.v[3 + k] = e1[3 * id + k];
+                t.v[6 + k] = e2[3 * id + k];
+            }
+            t.id = id;
+            tris[i] = t;
         }
-        t.id = id;
-        tris[i] = t;
+        if (i >= n) continue;
         for (int k = 0; k < 3; ++k) {
             by_id[9 * i + k] = v0[3 * i + k];
             by_id[9 * i + 3 + k] = e1[3 * i + k];
@@ -311,8 +319,9 @@ extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, c
     if (s->n_tri == 0) return EF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = s->n_tri;
-    update_tris_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(
-        s->tris, s->tris_by_id, s->normals, s->leaf_order, v0, e1, e2, normals, n);
+    const int64_t nm = std::max(n, s->n_refs);
+    update_tris_kernel<<<(int)std::min<int64_t>((nm + 255) / 256, 148 * 8), 256, 0, st>>>(
+        s->tris, s->tris_by_id, s->normals, s->leaf_order, v0, e1, e2, normals, n, s->n_refs);
     count_launch();
     const int levels = (int)s->level_start.size() - 1;
     for (int l = levels - 1; l >= 0; --l) {

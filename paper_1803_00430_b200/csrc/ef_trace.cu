@@ -742,7 +742,7 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         }();
         const bool big = force_big >= 0 ? force_big == 1
                                          : (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
-                                                   s->n_tri * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
+                                                   s->n_refs * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
         if (s->n_bands <= 4)
             e = dispatch<4>(brute, big, cfg->order, P, st);
         else
