@@ -222,15 +222,15 @@ int ef_trace(const ef_scene* scene, const ef_trace_config* cfg, const double* sr
  * One process per GPU, rays sharded by global index (ray0).  Instead of a
  * local (n_sources, ...) histogram followed by a reduce-scatter, every splat
  * of global source g is added straight into the block g % sources_per_rank
- * of rank g / sources_per_rank through DEVICE pointer tables (one entry per
- * rank): hist_peers[r] -> (sources_per_rank, n_bins, n_bands, nk) f32,
- * dir_peers[r] -> (sources_per_rank, n_bands, nk) f32, mapped with
- * ef_peer_open (remote atomics over NVLink/NVSwitch).  The blocks are
- * ACCUMULATED and owned by their rank: clear_outputs clears only the local
- * stats / sum_t, and the caller orders "owner zeroed" before and "all ranks
- * done" after the launch (distributed.PeerHistograms double-buffers so one
- * barrier per frame suffices).  Replaces bench.py's ef_trace +
- * reduce_scatter_tensor pair. */
+ * of rank g / sources_per_rank: hist_peers / dir_peers are HOST arrays of
+ * n_sources / sources_per_rank (<= 8) DEVICE pointers, rank r's entries
+ * -> (sources_per_rank, n_bins, n_bands, nk) f32 and
+ * (sources_per_rank, n_bands, nk) f32, mapped with ef_peer_open (remote
+ * atomics over NVLink/NVSwitch).  The blocks are ACCUMULATED and owned by
+ * their rank: clear_outputs clears only the local stats / sum_t, and the
+ * caller orders "owner zeroed" before and "all ranks done" after the launch
+ * (distributed.PeerHistograms double-buffers so one barrier per frame
+ * suffices).  Replaces bench.py's ef_trace + reduce_scatter_tensor pair. */
 int ef_trace_fused(const ef_scene* scene, const ef_trace_config* cfg, const double* src_pos,
                    const uint32_t* src_key, const uint32_t* ray_ids, float* const* hist_peers,
                    float* const* dir_peers, int32_t sources_per_rank, unsigned long long* stats,

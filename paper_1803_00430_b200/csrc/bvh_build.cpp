@@ -387,9 +387,9 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
         GpuNode g;
         std::memset(&g, 0, sizeof g);
         for (int c = 0; c < 4; ++c) {
-            // lo = +inf, hi = -inf: both sign-selected planes give t_near = +inf
+            // lo = hi = +inf: misses in the slab test (ef_device.cuh slab_key)
             g.lox[c] = g.loy[c] = g.loz[c] = INFINITY;
-            g.hix[c] = g.hiy[c] = g.hiz[c] = -INFINITY;
+            g.hix[c] = g.hiy[c] = g.hiz[c] = INFINITY;
             g.child[c] = kEmptyChild;
         }
         return g;

@@ -266,7 +266,7 @@ __global__ void collapse_kernel(int l, int* lvl, int* cnt, int* src, GpuNode* __
             g.pad[k] = 0;
             if (k >= nc) {
                 g.lox[k] = g.loy[k] = g.loz[k] = INFINITY;
-                g.hix[k] = g.hiy[k] = g.hiz[k] = -INFINITY;
+                g.hix[k] = g.hiy[k] = g.hiz[k] = INFINITY;
                 g.child[k] = kEmptyChild;
                 continue;
             }

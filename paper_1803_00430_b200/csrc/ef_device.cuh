@@ -230,10 +230,26 @@ __device__ __forceinline__ bool mt_hit(double ox, double oy, double oz, double d
     return t > t_min && t <= t_hi;
 }
 
-// Conservative slab test of one child box from its sign-selected near/far
-// planes; returns a sortable key (t_near bits with the low two bits replaced
-// by the child slot; t_near >= 0 so unsigned order == float order) or
-// 0xffffffff on a miss.  Empty slots hold lo = +inf, hi = -inf and miss.
+// Conservative slab test of one child box; returns a sortable key (t_near
+// bits with the low two bits replaced by the child slot; t_near >= 0 so
+// unsigned order == float order) or 0xffffffff on a miss.  Two equivalent
+// forms: slab_key_minmax evaluates both planes of an axis and orders them
+// (all seven loads of a node then use immediate offsets: fewer instructions),
+// slab_key takes the ray's sign-selected near/far planes (fewer registers).
+// Empty slots hold lo = hi = +inf: on an axis of positive direction t_near
+// = +inf, and with every direction component negative t_far = -inf, so they
+// miss as long as tmax is finite (closest_bvh clamps it to 1e38).
+__device__ __forceinline__ uint32_t slab_key_minmax(const RayF& r, float lx, float hx, float ly,
+                                                    float hy, float lz, float hz, float tmin,
+                                                    float tmax, uint32_t slot) {
+    const float ax = __fmaf_rn(lx, r.ix, -r.ox), bx = __fmaf_rn(hx, r.ix, -r.ox);
+    const float ay = __fmaf_rn(ly, r.iy, -r.oy), by = __fmaf_rn(hy, r.iy, -r.oy);
+    const float az = __fmaf_rn(lz, r.iz, -r.oz), bz = __fmaf_rn(hz, r.iz, -r.oz);
+    const float tn = fmax3f(fminf(ax, bx), fminf(ay, by), fmaxf(fminf(az, bz), tmin));
+    const float tf = fmin3f(fmaxf(ax, bx), fmaxf(ay, by), fminf(fmaxf(az, bz), tmax));
+    return tn <= __fmul_rn(tf, 1.0000038f) ? ((__float_as_uint(tn) & ~3u) | slot) : 0xffffffffu;
+}
+
 __device__ __forceinline__ uint32_t slab_key(const RayF& r, float nx, float fx, float ny, float fy,
                                              float nz, float fz, float tmin, float tmax,
                                              uint32_t slot) {
@@ -305,19 +321,19 @@ struct TravStack {
 // the tree and of the traversal order.  While-while form
 // (Aila & Laine 2009): each lane descends through inner nodes (nearest child
 // first, packed-key sorting network, farther hits pushed) until it holds a
-// leaf, so the expensive f64 leaf tests of a warp run together.  Nodes
-// [0, n_smem) are read from the shared-memory copy of the top of the tree.
+// leaf, so the expensive f64 leaf tests of a warp run together.  MINMAX
+// selects the slab form (slab_key_minmax / slab_key).
+template <bool MINMAX = true>
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
-                                           double t_max, const float4* s_nodes, int n_smem,
-                                           uint32_t& n_nodes, uint32_t& n_tris,
+                                           double t_max, uint32_t& n_nodes, uint32_t& n_tris,
                                            uint2* s_stack = nullptr, int s_depth = 0,
                                            bool any_hit = false) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
-    float tb = __double2float_ru(t_max);
+    float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
     TravStack st;
     st.s = s_stack;
     st.stride = blockDim.x;
@@ -329,25 +345,27 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
         while (node >= 0) {
             EF_PHASE_T0(tv);
             ++n_nodes;
-            float4 nx, fx, ny, fy, nz, fz;
+            const float4* q = reinterpret_cast<const float4*>(nodes + node);
+            uint32_t k0, k1, k2, k3;
             int4 ch;
-            if (node < n_smem) {   // top of the tree staged in shared memory
-                const float4* q = s_nodes + 8 * node;
-                nx = q[r.nx]; fx = q[r.nx ^ 1];
-                ny = q[r.ny]; fy = q[r.ny ^ 1];
-                nz = q[r.nz]; fz = q[r.nz ^ 1];
-                ch = *reinterpret_cast<const int4*>(q + 6);
-            } else {
-                const float4* q = reinterpret_cast<const float4*>(nodes + node);
-                nx = __ldg(q + r.nx); fx = __ldg(q + (r.nx ^ 1));
-                ny = __ldg(q + r.ny); fy = __ldg(q + (r.ny ^ 1));
-                nz = __ldg(q + r.nz); fz = __ldg(q + (r.nz ^ 1));
+            if (MINMAX) {
+                const float4 lx = __ldg(q + 0), hx = __ldg(q + 1), ly = __ldg(q + 2),
+                             hy = __ldg(q + 3), lz = __ldg(q + 4), hz = __ldg(q + 5);
                 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
+                k0 = slab_key_minmax(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tminf, tb, 0u);
+                k1 = slab_key_minmax(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tminf, tb, 1u);
+                k2 = slab_key_minmax(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tminf, tb, 2u);
+                k3 = slab_key_minmax(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tminf, tb, 3u);
+            } else {
+                const float4 nx = __ldg(q + r.nx), fx = __ldg(q + (r.nx ^ 1));
+                const float4 ny = __ldg(q + r.ny), fy = __ldg(q + (r.ny ^ 1));
+                const float4 nz = __ldg(q + r.nz), fz = __ldg(q + (r.nz ^ 1));
+                ch = __ldg(reinterpret_cast<const int4*>(q + 6));
+                k0 = slab_key(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tminf, tb, 0u);
+                k1 = slab_key(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tminf, tb, 1u);
+                k2 = slab_key(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tminf, tb, 2u);
+                k3 = slab_key(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tminf, tb, 3u);
             }
-            uint32_t k0 = slab_key(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tminf, tb, 0u);
-            uint32_t k1 = slab_key(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tminf, tb, 1u);
-            uint32_t k2 = slab_key(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tminf, tb, 2u);
-            uint32_t k3 = slab_key(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tminf, tb, 3u);
             kswap(k0, k1);
             kswap(k2, k3);
             kswap(k0, k2);
@@ -402,7 +420,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max) {
     uint32_t a = 0, b = 0;
-    return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, nullptr, 0, a, b);
+    return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, a, b);
 }
 
 // ------------------------------------------------------------------ SH ----

@@ -27,21 +27,12 @@ constexpr int kBigThreads = 768;
 constexpr int64_t kBigSceneBytes = 4ll << 20;
 template <int THREADS>
 constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
-// Shared-memory copy of the top of the tree: measured on B200 (C2/C3/C5) to
-// lose to leaving the space to L1 (C5 3.34 vs 2.93 G seg/s at 0 vs 128 KB,
-// C2 flat), so off by default.
-constexpr size_t kNodeCacheBytes = 0;
-
-// shared-memory node cache size; EF_NODE_CACHE_KB overrides (tuning only)
-static size_t node_cache_bytes() {
-    static size_t v = [] {
-        const char* e = std::getenv("EF_NODE_CACHE_KB");
-        return e ? (size_t)std::atoi(e) * 1024 : kNodeCacheBytes;
-    }();
-    return v;
-}
+// (A shared-memory copy of the top of the tree measured slower than leaving
+// the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
+// removed; profiles/r01_node_cache_sweep.txt.)
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr int kMaxSourcesPerLaunch = 256;
+constexpr int kMaxRanks = 8;   // GPUs of one node reachable by ef_trace_fused
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
@@ -81,12 +72,10 @@ struct TraceParams {
     int32_t n_bins, max_bounces;
     double bin_len, lx, ly, lz, r2;
     float e0;
-    float* H;
-    float* Dir;
-    // fused multi-GPU accumulation (ef_trace_fused): histogram / direct blocks
-    // of global source g live on rank g / spr at block g % spr; null = H/Dir
-    float* const* Hp;
-    float* const* Dp;
+    // histogram / direct-sound blocks: global source g lives on rank g / spr
+    // at block g % spr (ef_trace: one "rank", this process's H and Dir)
+    float* Hp[kMaxRanks];
+    float* Dp[kMaxRanks];
     int32_t spr;
     int32_t src0;           // global index of this launch's source 0
     unsigned long long* stats;
@@ -95,7 +84,6 @@ struct TraceParams {
     int32_t* path_ids;
     unsigned long long* counter;
     unsigned long long total;
-    int32_t n_smem_nodes;   // BVH nodes [0, n) staged in shared memory
     int32_t rain;           // diffuse rain (next-event estimation)
     const float* fr;        // (n_mat, nb) diffusely reflected fraction (1-a)*s, f32
     int32_t er_max_order;   // arrivals of order 1..er_max_order -> ER list
@@ -134,8 +122,8 @@ __device__ __forceinline__ void flush_stats(LaneStats& ls, unsigned int* s_stats
 // (its histogram or direct-sound block is `per` floats).  Remote atomics go
 // over NVLink to the owning GPU, so the frame's reduce-scatter happens inside
 // the trace kernel, splat by splat.
-__device__ __forceinline__ float* peer_block(float* const* tab, const TraceParams& P, int src,
-                                             size_t per) {
+__device__ __forceinline__ float* peer_block(float* const (&tab)[kMaxRanks], const TraceParams& P,
+                                             int src, size_t per) {
     const int g = P.src0 + src;
     const int o = g / P.spr;
     return tab[o] + (size_t)(g - o * P.spr) * per;
@@ -155,7 +143,7 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
     float* dst = nullptr;
     if (order == 0) {
         ls.c[EF_ST_DIRECT]++;
-        dst = P.Dp ? peer_block(P.Dp, P, src, (size_t)nb * NK) : P.Dir + (size_t)src * nb * NK;
+        dst = peer_block(P.Dp, P, src, (size_t)nb * NK);
     } else if (order <= P.er_max_order) {
         const unsigned int slot = atomicAdd(P.er_count, 1u);
         if (slot < (unsigned int)P.er_cap) {
@@ -175,8 +163,7 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
     } else {
         const double q = dist / P.bin_len;
         if (q < (double)P.n_bins)
-            dst = (P.Hp ? peer_block(P.Hp, P, src, (size_t)P.n_bins * nb * NK)
-                        : P.H + (size_t)src * P.n_bins * nb * NK) + (size_t)q * nb * NK;
+            dst = peer_block(P.Hp, P, src, (size_t)P.n_bins * nb * NK) + (size_t)q * nb * NK;
         else
             ls.c[EF_ST_DROPPED]++;
     }
@@ -209,11 +196,6 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     // traversal stacks (kSmemStack entries per thread), then the node cache
     uint2* s_stack = reinterpret_cast<uint2*>(
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
-    float4* s_nodes = reinterpret_cast<float4*>(s_stack + (BRUTE ? 0 : smem_stack_depth<THREADS>() * THREADS));
-    if (!BRUTE) {
-        const float4* g = reinterpret_cast<const float4*>(P.nodes);
-        for (int i = threadIdx.x; i < 8 * P.n_smem_nodes; i += blockDim.x) s_nodes[i] = __ldg(g + i);
-    }
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0u;
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
     if (BRUTE)
@@ -284,8 +266,8 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             ls.c[EF_ST_TRIS] += P.n_tri;
         }
         else
-            h = closest_bvh(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY, s_nodes,
-                            P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
+            h = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY,
+                            ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
                             s_stack + threadIdx.x, smem_stack_depth<THREADS>());
         const bool hit = h.id != INT32_MAX;
         EF_PHASE_T0(tsh);
@@ -347,8 +329,8 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                     if (BRUTE) {
                         sh = closest_brute(s_tri, P.n_tri, ox, oy, oz, ex, ey, ez, kRayEps, limit);
                     } else {
-                        sh = closest_bvh(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit, s_nodes,
-                                         P.n_smem_nodes, ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
+                        sh = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit,
+                                         ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
                                          s_stack + threadIdx.x, smem_stack_depth<THREADS>(), true);
                     }
                     if (sh.id == INT32_MAX) {
@@ -419,8 +401,7 @@ static int sm_count() {
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
 static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
-                  (BRUTE ? 0 : (size_t)P.n_smem_nodes * sizeof(GpuNode) +
-                                   (size_t)smem_stack_depth<THREADS>() * THREADS * sizeof(uint2));
+                  (BRUTE ? 0 : (size_t)smem_stack_depth<THREADS>() * THREADS * sizeof(uint2));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
@@ -642,8 +623,9 @@ extern "C" int ef_eval_sh_batch(const double* dirs, int64_t n, int32_t order, do
 
 namespace {
 
-// ef_trace and ef_trace_fused: either local H/Dir, or the peer tables Hp/Dp
-// with `spr` sources per rank (H = Dir = null).
+// ef_trace and ef_trace_fused: either local H/Dir, or the ranks' blocks
+// Hp/Dp (host arrays of n_ranks device pointers) with `spr` sources per rank
+// (H = Dir = null).
 int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_pos,
                const uint32_t* src_key, const uint32_t* ray_ids, float* H, float* Dir,
                float* const* Hp, float* const* Dp, int32_t spr, unsigned long long* stats,
@@ -662,8 +644,9 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
     const bool fused = Hp != nullptr;
     if (!src_pos || !stats || !sum_t || (fused ? !Dp : (!H || !Dir)))
         return set_error(EF_EINVAL, "ef_trace: null buffer");
-    if (fused && (spr < 1 || cfg->n_sources % spr != 0))
-        return set_error(EF_EINVAL, "ef_trace_fused: sources_per_rank must divide n_sources");
+    if (fused && (spr < 1 || cfg->n_sources % spr != 0 || cfg->n_sources / spr > kMaxRanks))
+        return set_error(EF_EINVAL, "ef_trace_fused: sources_per_rank must divide n_sources "
+                                    "into at most 8 ranks");
     if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_trace: empty scene is handled by the host");
     const bool brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= kBruteMaxTris);
     if (brute && s->n_tri > 2048) return set_error(EF_EINVAL, "ef_trace: all-pairs mode supports <= 2048 triangles");
@@ -716,12 +699,20 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.lz = cfg->listener[2];
         P.r2 = cfg->radius * cfg->radius;
         P.e0 = cfg->e0;
-        P.H = fused ? nullptr : H + (size_t)s0 * cfg->n_bins * s->n_bands * nk;
-        P.Dir = fused ? nullptr : Dir + (size_t)s0 * s->n_bands * nk;
-        P.Hp = Hp;
-        P.Dp = fused ? Dp : nullptr;
-        P.spr = fused ? spr : 1;
-        P.src0 = s0;
+        if (fused) {
+            for (int k = 0; k < kMaxRanks; ++k) {
+                P.Hp[k] = k < cfg->n_sources / spr ? Hp[k] : nullptr;
+                P.Dp[k] = k < cfg->n_sources / spr ? Dp[k] : nullptr;
+            }
+            P.spr = spr;
+            P.src0 = s0;
+        } else {   // one rank owning every source of this launch
+            for (int k = 0; k < kMaxRanks; ++k) P.Hp[k] = P.Dp[k] = nullptr;
+            P.Hp[0] = H + (size_t)s0 * cfg->n_bins * s->n_bands * nk;
+            P.Dp[0] = Dir + (size_t)s0 * s->n_bands * nk;
+            P.spr = ns;
+            P.src0 = 0;
+        }
         P.stats = stats + (size_t)s0 * EF_ST_COUNT;
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
@@ -735,7 +726,6 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.er_cap = cfg->er_capacity;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
-        P.n_smem_nodes = brute ? 0 : (int32_t)std::min<int64_t>(s->n_nodes, node_cache_bytes() / sizeof(GpuNode));
         static const int force_big = [] {
             const char* e = std::getenv("EF_TRACE_BIG");   // tuning only: 0 / 1
             return e ? std::atoi(e) : -1;

@@ -73,9 +73,8 @@ class _CudaPeerBackend:
         _lib.lib().ef_peer_free(ptr)
 
     def table(self, ptrs):
-        from . import _lib
-        t = _lib.torch()
-        return t.tensor([int(p) for p in ptrs], dtype=t.int64, device=_lib.device())
+        import ctypes
+        return (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])   # host array of device pointers
 
     def view(self, ptr, shape):
         from . import _lib
@@ -92,7 +91,8 @@ class PeerHistograms:
     Rank r owns sources [r*S/N, (r+1)*S/N) (owned_sources).  Its histogram
     and direct-sound blocks are allocated here (ef_peer_alloc), the CUDA IPC
     handles are exchanged once (all_gather_object), and every rank maps every
-    other rank's blocks (ef_peer_open) into two pointer tables.  The trace
+    other rank's blocks (ef_peer_open) into two pointer tables (host arrays
+    of device pointers, passed to the kernel by value).  The trace
     kernels of all ranks (FrameTracer.trace_fused -> ef_trace_fused) then add
     each splat straight into the owner's block over NVLink/NVSwitch: the
     reduce-scatter happens inside the trace, with no NCCL call after it.
@@ -143,7 +143,8 @@ class PeerHistograms:
         self._D = [be.view(self._own[p][1][0], self.shape_d) for p in range(2)]
 
     def tables(self, frame: int):
-        """(hist table, dir table) device pointer arrays for frame's parity."""
+        """(hist table, dir table) pointer arrays (one device pointer per rank)
+        for frame's parity."""
         return self._tab[frame & 1]
 
     def block(self, frame: int):
@@ -194,8 +195,9 @@ class EmulatedPeers:
                     for _ in range(n_ranks)] for _ in range(2)]
         self._D = [[t.zeros((spr, n_bands, nk), dtype=t.float32, device=dev)
                     for _ in range(n_ranks)] for _ in range(2)]
-        self._tab = [(t.tensor([x.data_ptr() for x in self._H[p]], dtype=t.int64, device=dev),
-                      t.tensor([x.data_ptr() for x in self._D[p]], dtype=t.int64, device=dev))
+        import ctypes
+        arr = ctypes.c_void_p * n_ranks
+        self._tab = [(arr(*[x.data_ptr() for x in self._H[p]]), arr(*[x.data_ptr() for x in self._D[p]]))
                      for p in range(2)]
 
     def tables(self, frame: int):

@@ -12,6 +12,8 @@ H[source, bin, band, sh] (float32).
 """
 from __future__ import annotations
 
+import ctypes
+
 import math
 from dataclasses import dataclass, field
 
@@ -257,7 +259,8 @@ class FrameTracer:
         tab_h, tab_d = peers.tables(frame if slot is None else slot)
         _lib.check(_lib.lib().ef_trace_fused(
             self._handle, cfg, _lib.ptr(self.src_pos), _lib.ptr(self.src_key), _lib.ptr(ids),
-            _lib.ptr(tab_h), _lib.ptr(tab_d), peers.sources_per_rank, _lib.ptr(self.stats),
+            ctypes.cast(tab_h, ctypes.c_void_p), ctypes.cast(tab_d, ctypes.c_void_p),
+            peers.sources_per_rank, _lib.ptr(self.stats),
             _lib.ptr(self.sum_t), _lib.ptr(self.path_nseg), _lib.ptr(self.path_ids),
             _lib.stream_handle(stream)))
 
