@@ -60,36 +60,52 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region:
+    ONE `nvidia-smi -lms` process (the profiling recipe's clocks line),
+    started before the region (first sample awaited) and stopped after, so
+    no per-sample process launch competes with the timed launches."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period_ms=100):
         self.index = index
+        self.period_ms = period_ms
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                        "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._p = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self._p.stdout:
+                try:
+                    sm, smax, reasons = [x.strip() for x in line.split(",")]
+                    self.samples.append((float(sm), float(smax), int(reasons, 16)))
+                    first.set()
+                except ValueError:
+                    pass
+
+        self._t = threading.Thread(target=reader, daemon=True)
         self._t.start()
+        first.wait(5.0)
         return self
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                sm, smax, reasons = [x.strip() for x in out.split(",")]
-                self.samples.append((float(sm), float(smax), int(reasons, 16)))
-            except Exception:
-                pass
-            self._stop.wait(0.1)
-
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._p.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -324,14 +340,23 @@ def run_gpu(args, w, metric, unit):
     Q_host = torch.empty(tuple(an.src_params.shape), dtype=torch.float64).pin_memory()
     e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.fill_(i & 0xff)
-        e_starts[i].record(stream)
+
+    def e2e_step():
         tr.src_pos.copy_(src_host, non_blocking=True)
         step()
         P_host.copy_(an.params, non_blocking=True)
         Q_host.copy_(an.src_params, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    host_t0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        e_starts[i].record(stream)
+        e2e_step()
         e_ends[i].record(stream)
+    host_enqueue_ms = (time.perf_counter() - host_t0) * 1e3 / args.steps
     torch.cuda.synchronize()
     e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
     h2d = src_host.numel() * 8
@@ -370,7 +395,8 @@ def run_gpu(args, w, metric, unit):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(args, w, world),
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps,
+                    "host_enqueue_ms_per_step": host_enqueue_ms},
             "gpu_launches": int(n_launch),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
