@@ -2,9 +2,10 @@
 
     python tools/summarize_ncu.py gpurun_out/launches.csv gpurun_out/prof_trace.ncu-rep profiles/r01_c2
 
-Writes <prefix>_launches.txt (per-kernel device time, share of the step),
-<prefix>_trace_full.txt (key metrics of the captured kernel) and
-profiles/traffic_<config>.json (DRAM bytes per launch, read by bench.py)."""
+Writes <prefix>_launches.txt (per-kernel device time, share of the step;
+skipped when the launch list is ""), <prefix>_full.txt (key metrics of the
+captured kernel) and profiles/traffic_<config>.json (DRAM bytes per launch,
+read by bench.py)."""
 import collections
 import csv
 import json
@@ -53,7 +54,7 @@ def raw(rep):
 def main():
     lpath, rep, prefix = sys.argv[1:4]
     config = sys.argv[4] if len(sys.argv) > 4 else "c2"
-    d = launches(lpath)
+    d = launches(lpath) if lpath else {}
     tot = sum(sum(v) / len(v) for k, v in d.items() if "ef::" in k)
     lines = ["kernel | launches | mean device time (us) | share of the library's step time",
              "---|---|---|---"]
@@ -61,15 +62,16 @@ def main():
         m = sum(v) / len(v) / 1e3
         share = f"{100 * m * 1e3 / tot:.1f}%" if "ef::" in k else "(torch / bench plumbing)"
         lines.append(f"{k[:70]} | {len(v)} | {m:.1f} | {share}")
-    open(prefix + "_launches.txt", "w").write(
-        "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n"
-        + "\n".join(lines) + "\n")
+    if d:
+        open(prefix + "_launches.txt", "w").write(
+            "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n"
+            + "\n".join(lines) + "\n")
     m, name = raw(rep)
     body = [f"# ncu --set full --clock-control none, kernel: {name}"]
     for k in KEYS:
         if k in m:
             body.append(f"{k} = {m[k][0]} {m[k][1]}")
-    open(prefix + "_trace_full.txt", "w").write("\n".join(body) + "\n")
+    open(prefix + "_full.txt", "w").write("\n".join(body) + "\n")
     rd = float(m["dram__bytes_read.sum"][0].replace(",", ""))
     wr = float(m["dram__bytes_write.sum"][0].replace(",", ""))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -77,7 +79,7 @@ def main():
     wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
     os.makedirs("profiles", exist_ok=True)
     json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": rep,
-               "note": "one ncu --set full capture of trace_kernel"},
+               "note": f"one ncu --set full capture of {name.split('(')[0]}"},
               open(os.path.join("profiles", f"traffic_{config}.json"), "w"), indent=1)
     print("\n".join(lines))
     print("\n".join(body))
