@@ -26,7 +26,18 @@ constexpr int kSmallThreads = 512;
 constexpr int kBigThreads = 768;
 constexpr int64_t kBigSceneBytes = 4ll << 20;
 template <int THREADS>
-constexpr int smem_stack_depth() { return THREADS <= 512 ? 16 : 12; }
+constexpr int smem_stack_depth_default() { return THREADS <= 512 ? 16 : 12; }
+// EF_SMEM_STACK overrides the shared stack entries per thread (tuning; the
+// rest of the stack lives in local memory)
+template <int THREADS>
+static int smem_stack_depth_host() {
+    static const int v = [] {
+        const char* e = std::getenv("EF_SMEM_STACK");
+        const int d = e ? std::atoi(e) : smem_stack_depth_default<THREADS>();
+        return std::max(0, std::min(d, kSmemStack));
+    }();
+    return v;
+}
 // (A shared-memory copy of the top of the tree measured slower than leaving
 // the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
 // removed; profiles/r01_node_cache_sweep.txt.)
@@ -91,6 +102,7 @@ struct TraceParams {
     unsigned int* er_count;
     int64_t er_cap;
     int32_t timing;         // debug: path_ids rows get (t0, t1, smid, nseg)
+    int32_t smem_stack;     // traversal stack entries per thread kept in shared memory
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         else
             h = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY,
                             ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
-                            s_stack + threadIdx.x, smem_stack_depth<THREADS>());
+                            s_stack + threadIdx.x, P.smem_stack);
         const bool hit = h.id != INT32_MAX;
         EF_PHASE_T0(tsh);
         if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                     } else {
                         sh = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit,
                                          ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
-                                         s_stack + threadIdx.x, smem_stack_depth<THREADS>(), true);
+                                         s_stack + threadIdx.x, P.smem_stack, true);
                     }
                     if (sh.id == INT32_MAX) {
                         const float gf = (float)(cosv * P.r2 / d2);
@@ -399,9 +411,11 @@ static int sm_count() {
 }
 
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
-static cudaError_t launch_trace(const TraceParams& P, cudaStream_t st) {
+static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
+    TraceParams P = P0;
+    P.smem_stack = smem_stack_depth_host<THREADS>();
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
-                  (BRUTE ? 0 : (size_t)smem_stack_depth<THREADS>() * THREADS * sizeof(uint2));
+                  (BRUTE ? 0 : (size_t)P.smem_stack * THREADS * sizeof(uint2));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
