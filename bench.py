@@ -327,7 +327,8 @@ def run_gpu(args, w, metric, unit):
     if world > 1:
         dist.barrier()
     n_launch = _lib.launch_count() - n_launch0
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(step_ms)
     k_ms = sum(a.elapsed_time(b) for a, b in kev)
     segs_per_step = int(seg_total.item()) / args.steps   # this rank's mean segments per frame
 
@@ -403,6 +404,8 @@ def run_gpu(args, w, metric, unit):
                          "kernel": "trace_kernel", "kernel_ms_per_launch": avg_k_s * 1e3,
                          "algorithmic_bytes_per_segment": bseg,
                          "segments_per_launch": round(segs_per_step)},
+            "step_ms_quantiles": {q: float(np.percentile(step_ms, p)) for q, p in
+                                  (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))},
             "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
             "clocks": clocks.summary()}
     if world == 1 and not args.no_cpu_baseline:

@@ -2,6 +2,7 @@
 // every f64 expression below is evaluated exactly as written, matching the
 // reference's numpy evaluation order bit-for-bit).
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -295,12 +296,50 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
     }
 }
 
-// Traversal stack: entries [0, kSmemStack) live in shared memory (i-major,
-// one column per thread: conflict-free and immune to L1 thrashing by node and
+// Traversal stack: entries [0, depth) live in shared memory (i-major, one
+// column per thread: conflict-free and immune to L1 thrashing by node and
 // triangle traffic), deeper entries in local memory.  Entry = (node, key).
+// The scalars stay in registers and the shared column is addressed through
+// a 32-bit shared-window address (st.shared / ld.shared), so a push is one
+// STS instead of a generic store plus local-memory bookkeeping.
 constexpr int kSmemStack = 16;   // max shared entries per thread (runtime depth <= this)
 
 struct TravStack {
+    uint32_t sbase;  // shared address of this thread's column
+    uint32_t sstep;  // bytes between consecutive entries of a column (8 * blockDim.x)
+    int depth;       // shared entries per thread
+    int sp;
+    uint2* l;        // local-memory overflow array (kept outside this struct so
+                     // the scalars above can live in registers)
+
+    __device__ __forceinline__ void push(int32_t node, uint32_t key) {
+        if (sp < depth) {
+            // volatile asm keeps push/pop order; no memory clobber, so global
+            // loads (nodes, triangles) still schedule freely around it
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sbase + (uint32_t)sp * sstep),
+                         "r"((uint32_t)node), "r"(key));
+        } else {
+            l[sp] = make_uint2((uint32_t)node, key);
+        }
+        ++sp;
+    }
+    __device__ __forceinline__ uint2 top() const {
+        if (sp < depth) {
+            uint2 e;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
+                         : "r"(sbase + (uint32_t)sp * sstep));
+            return e;
+        }
+        return l[sp];
+    }
+};
+
+// The same stack with its scalars and overflow array in one local-memory
+// object and a generic pointer to the shared column.  Measured faster in the
+// register-starved 768-thread kernel on C3 (62.6 vs 72.5 ms per frame, the
+// register-resident form frees fewer registers than it costs there), slower
+// in the 512-thread one (C2 0.665 vs 0.649 ms).
+struct TravStackMem {
     uint2* s;        // shared column base (nullptr: local only)
     int stride;      // blockDim.x
     int depth;       // shared entries per thread
@@ -316,13 +355,30 @@ struct TravStack {
     __device__ __forceinline__ uint2 top() const { return sp < depth ? s[sp * stride] : l[sp]; }
 };
 
+__device__ __forceinline__ void init_stack(TravStack& st, uint2* overflow, uint2* s_stack,
+                                           int s_depth) {
+    st.l = overflow;
+    st.sbase = s_stack ? (uint32_t)__cvta_generic_to_shared(s_stack) : 0u;
+    st.sstep = 8u * blockDim.x;
+    st.depth = s_stack ? s_depth : 0;
+    st.sp = 0;
+}
+__device__ __forceinline__ void init_stack(TravStackMem& st, uint2*, uint2* s_stack, int s_depth) {
+    st.s = s_stack;
+    st.stride = blockDim.x;
+    st.depth = s_stack ? s_depth : 0;
+    st.sp = 0;
+}
+
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
 // equal t resolves to the lowest triangle id, so the answer is independent of
 // the tree and of the traversal order.  While-while form
 // (Aila & Laine 2009): each lane descends through inner nodes (nearest child
 // first, packed-key sorting network, farther hits pushed) until it holds a
 // leaf, so the expensive f64 leaf tests of a warp run together.  MINMAX
-// selects the slab form (slab_key_minmax / slab_key).
+// selects the forms measured faster in the 512-thread kernel (slab_key_minmax,
+// the register-resident TravStack) over those of the register-starved
+// 768-thread one (slab_key, TravStackMem).
 template <bool MINMAX = true>
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
@@ -334,11 +390,9 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
-    TravStack st;
-    st.s = s_stack;
-    st.stride = blockDim.x;
-    st.depth = s_stack ? s_depth : 0;
-    st.sp = 0;
+    uint2 overflow[kStackSize];   // TravStack's local overflow (unused by TravStackMem)
+    typename std::conditional<MINMAX, TravStack, TravStackMem>::type st;
+    init_stack(st, overflow, s_stack, s_depth);
     int32_t node = 0;
     bool done = false;
     for (;;) {
