@@ -155,10 +155,15 @@ struct RayF {
     int nx, ny, nz;      // float4 index of the near plane per axis (far = near ^ 1)
 };
 
+// 1/d for the slab test.  rcp.approx (<= 1 ulp, no slow path): an error in
+// 1/d scales every plane distance of that axis alike, far inside the slab
+// test's 3.8e-6 slack and the boxes' 1e-5 * scale padding.
 __device__ __forceinline__ float safe_inv(double d) {
     float f = (float)d;
     if (fabsf(f) < 1e-20f) f = copysignf(1e-20f, f);
-    return __frcp_rn(f);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
+    return r;
 }
 
 __device__ __forceinline__ RayF make_rayf(double ox, double oy, double oz, double dx, double dy,
