@@ -49,13 +49,31 @@ constexpr unsigned kFull = 0xffffffffu;
 // ---------------------------------------------------------------------------
 // all-pairs closest hit over triangles staged in shared memory (T <= 512),
 // ids ascending with a strict '<': ties go to the lowest id (scene.py:220)
+// All-pairs closest hit (scene.py:208-230 for <= 512 triangles): the exact
+// test of every triangle, lowest index on equal t.  Two triangles per step,
+// each tested against t_max alone, so their f64 chains are independent and
+// overlap; the running minimum is folded in afterwards in index order.
 __device__ __forceinline__ Hit closest_brute(const double* __restrict__ s_tri, int n, double ox,
                                              double oy, double oz, double dx, double dy, double dz,
                                              double t_min, double t_max) {
     Hit h{INFINITY, INT32_MAX};
-    for (int i = 0; i < n; ++i) {
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+        double ta, tb;
+        const bool ha = mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, t_max, ta);
+        const bool hb = mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * (i + 1), t_min, t_max, tb);
+        if (ha && ta < h.t) {
+            h.t = ta;
+            h.id = i;
+        }
+        if (hb && tb < h.t) {
+            h.t = tb;
+            h.id = i + 1;
+        }
+    }
+    if (i < n) {
         double t;
-        if (mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, fmin(t_max, h.t), t) && t < h.t) {
+        if (mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, t_max, t) && t < h.t) {
             h.t = t;
             h.id = i;
         }
@@ -414,8 +432,17 @@ template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
 static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     TraceParams P = P0;
     P.smem_stack = smem_stack_depth_host<THREADS>();
+    // Too few paths to give every SM a full CTA (C1: 4,096 paths): spread them
+    // over all SMs in smaller CTAs (>= one warp), so each path's latency-bound
+    // chain shares its SM with as few others as possible.
+    const long long sms = (long long)sm_count();
+    int block = THREADS;
+    if ((long long)P.total < sms * THREADS) {
+        const long long per = ((long long)P.total + sms - 1) / sms;
+        block = (int)std::min<long long>(THREADS, std::max<long long>(32, (per + 31) / 32 * 32));
+    }
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
-                  (BRUTE ? 0 : (size_t)P.smem_stack * THREADS * sizeof(uint2));
+                  (BRUTE ? 0 : (size_t)P.smem_stack * block * sizeof(uint2));
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
@@ -425,12 +452,11 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
         attr_done = true;
     }
     if (smem > kMaxTraceSmem) return cudaErrorInvalidValue;
-    // persistent grid: one 512-thread CTA per SM (__launch_bounds__(512, 1)
-    // and ~100 registers leave room for exactly one), no more warps than paths
-    long long want = (long long)sm_count();
-    long long need = ((long long)P.total + THREADS - 1) / THREADS;
-    int grid = (int)std::max(1LL, std::min(want, need));
-    kern<<<grid, THREADS, smem, st>>>(P);
+    // persistent grid: one CTA per SM (__launch_bounds__(THREADS, 1) and the
+    // register budget leave room for exactly one), no more warps than paths
+    const long long need = ((long long)P.total + block - 1) / block;
+    const int grid = (int)std::max(1LL, std::min(sms, need));
+    kern<<<grid, block, smem, st>>>(P);
     count_launch();
     return cudaGetLastError();
 }
