@@ -128,76 +128,180 @@ __device__ __forceinline__ float tap(const float* __restrict__ row, long long t,
     return __fmaf_rn(w, b - a, a);
 }
 
+// ---- bulk-copy (TMA engine) + mbarrier helpers, raw PTX for sm_100a
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// Stage buffer of one (source, band) job: 16 line windows of 512 samples,
+// each fetched 16-byte aligned (up to 3 extra samples at either end, and a
+// wrap of the ring splits it in two copies landing back to back).
+constexpr int kWin = kBlock + 8;
+constexpr int kStages = 3;   // jobs in flight: the current one and the next two
+constexpr size_t kRenderDynSmem = (size_t)kStages * kLines * kWin * sizeof(float);
+
+// Job (s, b)'s line windows: the window of line i starts at sample `start`
+// of its ring; it is fetched from the 16-byte aligned a0 <= start, in one
+// copy or, when it wraps the ring, two copies landing back to back.
+struct Window {
+    int a0, n1, n2;   // first copy [a0, a0 + n1) floats, second [0, n2) (0: none)
+};
+__device__ __forceinline__ Window window(int start, int L) {
+    Window w;
+    w.a0 = start & ~3;
+    const int end = start + kBlock;
+    if (end <= L) {
+        w.n1 = ((end + 3) & ~3) - w.a0;
+        w.n2 = 0;
+    } else {
+        w.n1 = L - w.a0;
+        w.n2 = (end - L + 3) & ~3;
+    }
+    return w;
+}
+
+// Thread 0: arm stage barrier `bar` with the job's byte count, then issue
+// the bulk copies of job (s, b) into `buf`; off[i] = window start in line i.
+__device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, float* buf, int* off,
+                                          uint32_t bar) {
+    const int L = A.line_len;
+    int start[kLines];
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int i = 0; i < kLines; ++i) {
+        start[i] = (int)((A.t - __ldg(A.m + s * kLines + i)) & (L - 1));
+        const Window w = window(start[i], L);
+        bytes += (uint32_t)(w.n1 + w.n2) * 4u;
+    }
+    mbar_expect_tx(bar, bytes);
+#pragma unroll
+    for (int i = 0; i < kLines; ++i) {
+        const Window w = window(start[i], L);
+        const float* row = A.lines + (((size_t)s * kBands + b) * kLines + i) * L;
+        const uint32_t dst = smem_addr(buf + i * kWin);
+        off[i] = start[i] - w.a0;
+        bulk_g2s(dst, row + w.a0, (uint32_t)w.n1 * 4u, bar);
+        if (w.n2) bulk_g2s(dst + (uint32_t)w.n1 * 4u, row, (uint32_t)w.n2 * 4u, bar);
+    }
+}
+
+// Persistent CTAs of 512 threads (thread = sample).  The FDN's delayed line
+// samples of each (source, band) job arrive by bulk copies (TMA engine) into
+// one of three shared-memory stages while earlier jobs compute: thread 0
+// issues job j+2's 16-24 copies, everyone waits on job j's mbarrier, reads
+// its line samples from shared memory, writes this block's line inputs and
+// accumulates the SH bus.  The read data is complete in shared memory before
+// any write of the job, so the ring's read/write aliasing needs no barrier;
+// one __syncthreads per job frees the stage for the copy two jobs later.
 __global__ void __launch_bounds__(kBlock, 2) render_kernel(AudioState A) {
+    extern __shared__ __align__(128) float s_buf[];   // kStages x kLines x kWin
+    __shared__ __align__(8) unsigned long long s_full[kStages];
+    __shared__ int s_off[kStages][kLines];
     __shared__ float s_M[kBands * kSh * kLines];
     __shared__ float s_Y[kSh];
     __shared__ float s_g[kBands * kLines];
-    __shared__ int s_m[kLines];
     __shared__ float s_gain[kBands];
     __shared__ int s_d[2];
     __shared__ float s_w[2];
     const int n = threadIdx.x;
     const long long t = A.t + n;
-    const int hmask = A.hist_len - 1, lmask = A.line_len - 1;
+    const int hmask = A.hist_len - 1;
     float bus[kSh];
 #pragma unroll
     for (int k = 0; k < kSh; ++k) bus[k] = 0.f;
-    for (int s = blockIdx.x; s < A.S; s += gridDim.x) {
-        for (int i = n; i < kBands * kSh * kLines; i += kBlock) s_M[i] = A.M[(size_t)s * kBands * kSh * kLines + i];
-        if (n < kSh) s_Y[n] = A.Y[s * kSh + n];
-        if (n < kBands * kLines) s_g[n] = A.g[(size_t)s * kBands * kLines + n];
-        if (n < kLines) s_m[n] = A.m[s * kLines + n];
-        if (n < kBands) s_gain[n] = A.gain[s * kBands + n];
-        if (n == 0) {
-            s_d[0] = A.d_int[s];
-            s_w[0] = A.d_w[s];
-            s_d[1] = A.p_int[s];
-            s_w[1] = A.p_w[s];
+    const int my_sources = blockIdx.x < A.S ? (A.S - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int jobs = kBands * my_sources;
+    if (n == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(smem_addr(&s_full[st]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int j = 0; j < kStages - 1 && j < jobs; ++j)
+            issue_job(A, blockIdx.x + (j / kBands) * gridDim.x, j % kBands,
+                      s_buf + (size_t)j * kLines * kWin, s_off[j], smem_addr(&s_full[j]));
+    }
+    __syncthreads();
+    float send[kBands];
+    for (int j = 0; j < jobs; ++j) {
+        const int s = blockIdx.x + (j / kBands) * gridDim.x;
+        const int b = j % kBands;
+        const int st = j % kStages;
+        const int ja = j + kStages - 1;   // prefetch into the stage job j - 1 freed
+        if (n == 0 && ja < jobs) {
+            const int st1 = ja % kStages;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_job(A, blockIdx.x + (ja / kBands) * gridDim.x, ja % kBands,
+                      s_buf + (size_t)st1 * kLines * kWin, s_off[st1], smem_addr(&s_full[st1]));
         }
-        __syncthreads();
-        const float* hs = A.hist + (size_t)s * kBands * A.hist_len;
-        // direct path: one tap per band, SH encode
-        float mono = 0.f;
-        float send[kBands];
-#pragma unroll
-        for (int b = 0; b < kBands; ++b) {
-            const float* row = hs + (size_t)b * A.hist_len;
-            mono = __fmaf_rn(s_gain[b], tap(row, t, s_d[0], s_w[0], hmask), mono);
-            send[b] = tap(row, t, s_d[1], s_w[1], hmask);
-        }
-#pragma unroll
-        for (int k = 0; k < kSh; ++k) bus[k] = __fmaf_rn(s_Y[k], mono, bus[k]);
-        // FDN, one band at a time: read every delayed line sample first
-        // (m_i > block, so all come from earlier blocks), barrier (a write
-        // slot of this block can alias another thread's read slot), then
-        // write this block's line inputs and accumulate the SH output
-        float* ls = A.lines + (size_t)s * kBands * kLines * A.line_len;
-#pragma unroll 1
-        for (int b = 0; b < kBands; ++b) {
-            float y[kLines];
-#pragma unroll
-            for (int i = 0; i < kLines; ++i)
-                y[i] = ls[((size_t)b * kLines + i) * A.line_len + ((t - s_m[i]) & lmask)];
+        if (b == 0) {
+            for (int i = n; i < kBands * kSh * kLines; i += kBlock) s_M[i] = A.M[(size_t)s * kBands * kSh * kLines + i];
+            if (n < kSh) s_Y[n] = A.Y[s * kSh + n];
+            if (n < kBands * kLines) s_g[n] = A.g[(size_t)s * kBands * kLines + n];
+            if (n < kBands) s_gain[n] = A.gain[s * kBands + n];
+            if (n == 32) {
+                s_d[0] = A.d_int[s];
+                s_w[0] = A.d_w[s];
+                s_d[1] = A.p_int[s];
+                s_w[1] = A.p_w[s];
+            }
             __syncthreads();
-            float sum = 0.f;
+            const float* hs = A.hist + (size_t)s * kBands * A.hist_len;
+            // direct path: one tap per band, SH encode
+            float mono = 0.f;
 #pragma unroll
-            for (int i = 0; i < kLines; ++i) {
-                sum = __fmaf_rn(s_g[b * kLines + i], y[i], sum);
+            for (int bb = 0; bb < kBands; ++bb) {
+                const float* row = hs + (size_t)bb * A.hist_len;
+                mono = __fmaf_rn(s_gain[bb], tap(row, t, s_d[0], s_w[0], hmask), mono);
+                send[bb] = tap(row, t, s_d[1], s_w[1], hmask);
             }
-            const float in = 0.25f * send[b] - (2.0f / kLines) * sum;   // Householder feedback
 #pragma unroll
-            for (int i = 0; i < kLines; ++i)
-                ls[((size_t)b * kLines + i) * A.line_len + (t & lmask)] = __fmaf_rn(s_g[b * kLines + i], y[i], in);
-            // line outputs -> SH bus through g_reverb,b * D_b * E
-#pragma unroll
-            for (int k = 0; k < kSh; ++k) {
-                float acc = bus[k];
-#pragma unroll
-                for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(s_M[(b * kSh + k) * kLines + i], y[i], acc);
-                bus[k] = acc;
-            }
+            for (int k = 0; k < kSh; ++k) bus[k] = __fmaf_rn(s_Y[k], mono, bus[k]);
         }
-        __syncthreads();
+        // stage `st` serves job j on its (j / kStages)-th use: phase parity
+        mbar_wait(smem_addr(&s_full[st]), (uint32_t)(j / kStages) & 1u);
+        const float* sb = s_buf + (size_t)st * kLines * kWin;
+        float y[kLines];
+#pragma unroll
+        for (int i = 0; i < kLines; ++i) y[i] = sb[i * kWin + s_off[st][i] + n];
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < kLines; ++i) sum = __fmaf_rn(s_g[b * kLines + i], y[i], sum);
+        const float in = 0.25f * send[b] - (2.0f / kLines) * sum;   // Householder feedback
+        float* ls = A.lines + ((size_t)s * kBands + b) * kLines * A.line_len;
+        const int w = (int)(t & (A.line_len - 1));
+#pragma unroll
+        for (int i = 0; i < kLines; ++i) ls[(size_t)i * A.line_len + w] = __fmaf_rn(s_g[b * kLines + i], y[i], in);
+        // line outputs -> SH bus through g_reverb,b * D_b * E
+#pragma unroll
+        for (int k = 0; k < kSh; ++k) {
+            float acc = bus[k];
+#pragma unroll
+            for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(s_M[(b * kSh + k) * kLines + i], y[i], acc);
+            bus[k] = acc;
+        }
+        __syncthreads();   // stage st free for job j + kStages; parameters free after band 3
     }
     for (int k = 0; k < kSh; ++k) A.partial[((size_t)blockIdx.x * kSh + k) * kBlock + n] = bus[k];
 }
@@ -333,7 +437,7 @@ extern "C" int ef_audio_create(const ef_audio_config* cfg, const float* sos, con
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    A.grid = std::min(S, 4 * sms);   // two 512-thread CTAs per SM, two waves
+    A.grid = std::min(S, 2 * sms);   // two resident 512-thread CTAs per SM, persistent
     cudaError_t e = cudaSuccess;
 #define UP(f, src, n) if (e == cudaSuccess) e = up(&A.f, src, (size_t)(n), A.bytes);
     UP(sos, sos, kBands * kBiquads * 5);
@@ -383,7 +487,14 @@ extern "C" int ef_audio_process(ef_audio* h, const float* x, float* bus_out, flo
     AudioState& A = h->A;
     const int xg = (A.S + (kXoverThreads / kBands) - 1) / (kXoverThreads / kBands);
     xover_kernel<<<xg, kXoverThreads, 0, st>>>(A, x);
-    render_kernel<<<A.grid, kBlock, 0, st>>>(A);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kRenderDynSmem);
+        if (e != cudaSuccess) return check_cuda(e, "render_kernel attributes");
+        attr = true;
+    }
+    render_kernel<<<A.grid, kBlock, kRenderDynSmem, st>>>(A);
     reduce_kernel<<<kSh, kBlock, 0, st>>>(A, bus_out);
     bus_kernel<<<1, 512, 0, st>>>(A, out);
     count_launch(4);
