@@ -150,6 +150,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -161,8 +164,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // each fetched 16-byte aligned (up to 3 extra samples at either end, and a
 // wrap of the ring splits it in two copies landing back to back).
 constexpr int kWin = kBlock + 8;
-constexpr int kStages = 3;   // jobs in flight: the current one and the next two
-constexpr size_t kRenderDynSmem = (size_t)kStages * kLines * kWin * sizeof(float);
+constexpr int kStages = 4;                         // jobs in flight
+constexpr int kStageM = kLines * kWin;             // band's line -> SH matrix (256 floats)
+constexpr int kStageG = kStageM + kSh * kLines;    // band's line gains (16 floats)
+constexpr int kStageFloats = kStageG + kLines;
+constexpr size_t kRenderDynSmem = (size_t)kStages * kStageFloats * sizeof(float);
+constexpr int kConsumerWarps = kBlock / 32;        // one sample per consumer thread
+constexpr int kRenderThreads = kBlock + 32;        // + one producer warp
 
 // Job (s, b)'s line windows: the window of line i starts at sample `start`
 // of its ring; it is fetched from the 16-byte aligned a0 <= start, in one
@@ -184,13 +192,14 @@ __device__ __forceinline__ Window window(int start, int L) {
     return w;
 }
 
-// Thread 0: arm stage barrier `bar` with the job's byte count, then issue
-// the bulk copies of job (s, b) into `buf`; off[i] = window start in line i.
+// Producer lane: arm stage barrier `bar` with the job's byte count, then
+// issue the bulk copies of job (s, b) into stage `buf`: the 16 line windows
+// (off[i] = window start in line i), the band's line -> SH matrix and gains.
 __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, float* buf, int* off,
                                           uint32_t bar) {
     const int L = A.line_len;
     int start[kLines];
-    uint32_t bytes = 0;
+    uint32_t bytes = (uint32_t)(kSh * kLines + kLines) * 4u;   // M_b and g_b
 #pragma unroll
     for (int i = 0; i < kLines; ++i) {
         start[i] = (int)((A.t - __ldg(A.m + s * kLines + i)) & (L - 1));
@@ -198,6 +207,9 @@ __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, flo
         bytes += (uint32_t)(w.n1 + w.n2) * 4u;
     }
     mbar_expect_tx(bar, bytes);
+    const size_t sb = (size_t)s * kBands + b;
+    bulk_g2s(smem_addr(buf + kStageM), A.M + sb * kSh * kLines, kSh * kLines * 4u, bar);
+    bulk_g2s(smem_addr(buf + kStageG), A.g + sb * kLines, kLines * 4u, bar);
 #pragma unroll
     for (int i = 0; i < kLines; ++i) {
         const Window w = window(start[i], L);
@@ -209,99 +221,99 @@ __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, flo
     }
 }
 
-// Persistent CTAs of 512 threads (thread = sample).  The FDN's delayed line
-// samples of each (source, band) job arrive by bulk copies (TMA engine) into
-// one of three shared-memory stages while earlier jobs compute: thread 0
-// issues job j+2's 16-24 copies, everyone waits on job j's mbarrier, reads
-// its line samples from shared memory, writes this block's line inputs and
-// accumulates the SH bus.  The read data is complete in shared memory before
-// any write of the job, so the ring's read/write aliasing needs no barrier;
-// one __syncthreads per job frees the stage for the copy two jobs later.
-__global__ void __launch_bounds__(kBlock, 2) render_kernel(AudioState A) {
-    extern __shared__ __align__(128) float s_buf[];   // kStages x kLines x kWin
+// Persistent CTAs, one per SM: 16 consumer warps (thread = sample) and one
+// producer warp.  Work is a sequence of (source, band) jobs.  The producer
+// lane fetches each job with bulk copies (the TMA engine: the 16 delayed
+// line windows, the band's line -> SH matrix and gains) into a 4-stage
+// shared-memory ring, waiting on the stage's "empty" mbarrier and arming its
+// "full" one; consumers wait on "full", run the band's FDN (line writes go
+// straight to global memory) and SH accumulation, and each warp arrives on
+// "empty".  No CTA-wide barrier: warps drift freely, the producer stays up
+// to four jobs ahead.  A job's reads are complete in shared memory before
+// it writes, so the ring's read/write aliasing is harmless.
+__global__ void __launch_bounds__(kRenderThreads, 1) render_kernel(AudioState A) {
+    extern __shared__ __align__(128) float s_buf[];   // kStages x kStageFloats
     __shared__ __align__(8) unsigned long long s_full[kStages];
+    __shared__ __align__(8) unsigned long long s_empty[kStages];
     __shared__ int s_off[kStages][kLines];
-    __shared__ float s_M[kBands * kSh * kLines];
-    __shared__ float s_Y[kSh];
-    __shared__ float s_g[kBands * kLines];
-    __shared__ float s_gain[kBands];
-    __shared__ int s_d[2];
-    __shared__ float s_w[2];
     const int n = threadIdx.x;
+    const int my_sources = blockIdx.x < A.S ? (A.S - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int jobs = kBands * my_sources;
+    if (n == 0) {
+        for (int st = 0; st < kStages; ++st) {
+            mbar_init(smem_addr(&s_full[st]), 1);
+            mbar_init(smem_addr(&s_empty[st]), kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (n >= kBlock) {   // ---- producer warp
+        if (n == kBlock) {
+            for (int j = 0; j < jobs; ++j) {
+                const int st = j % kStages;
+                const int use = j / kStages;
+                if (use > 0) mbar_wait(smem_addr(&s_empty[st]), (uint32_t)(use - 1) & 1u);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_job(A, blockIdx.x + (j / kBands) * gridDim.x, j % kBands,
+                          s_buf + (size_t)st * kStageFloats, s_off[st], smem_addr(&s_full[st]));
+            }
+        }
+        return;
+    }
+    // ---- consumers
+    const int lane = n & 31;
     const long long t = A.t + n;
     const int hmask = A.hist_len - 1;
     float bus[kSh];
 #pragma unroll
     for (int k = 0; k < kSh; ++k) bus[k] = 0.f;
-    const int my_sources = blockIdx.x < A.S ? (A.S - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int jobs = kBands * my_sources;
-    if (n == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(smem_addr(&s_full[st]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int j = 0; j < kStages - 1 && j < jobs; ++j)
-            issue_job(A, blockIdx.x + (j / kBands) * gridDim.x, j % kBands,
-                      s_buf + (size_t)j * kLines * kWin, s_off[j], smem_addr(&s_full[j]));
-    }
-    __syncthreads();
     float send[kBands];
     for (int j = 0; j < jobs; ++j) {
         const int s = blockIdx.x + (j / kBands) * gridDim.x;
         const int b = j % kBands;
         const int st = j % kStages;
-        const int ja = j + kStages - 1;   // prefetch into the stage job j - 1 freed
-        if (n == 0 && ja < jobs) {
-            const int st1 = ja % kStages;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_job(A, blockIdx.x + (ja / kBands) * gridDim.x, ja % kBands,
-                      s_buf + (size_t)st1 * kLines * kWin, s_off[st1], smem_addr(&s_full[st1]));
-        }
         if (b == 0) {
-            for (int i = n; i < kBands * kSh * kLines; i += kBlock) s_M[i] = A.M[(size_t)s * kBands * kSh * kLines + i];
-            if (n < kSh) s_Y[n] = A.Y[s * kSh + n];
-            if (n < kBands * kLines) s_g[n] = A.g[(size_t)s * kBands * kLines + n];
-            if (n < kBands) s_gain[n] = A.gain[s * kBands + n];
-            if (n == 32) {
-                s_d[0] = A.d_int[s];
-                s_w[0] = A.d_w[s];
-                s_d[1] = A.p_int[s];
-                s_w[1] = A.p_w[s];
-            }
-            __syncthreads();
-            const float* hs = A.hist + (size_t)s * kBands * A.hist_len;
             // direct path: one tap per band, SH encode
+            // (per-source scalars read by every thread: L1 broadcasts)
+            const float* hs = A.hist + (size_t)s * kBands * A.hist_len;
+            const int d0 = __ldg(A.d_int + s), d1 = __ldg(A.p_int + s);
+            const float w0 = __ldg(A.d_w + s), w1 = __ldg(A.p_w + s);
             float mono = 0.f;
 #pragma unroll
             for (int bb = 0; bb < kBands; ++bb) {
                 const float* row = hs + (size_t)bb * A.hist_len;
-                mono = __fmaf_rn(s_gain[bb], tap(row, t, s_d[0], s_w[0], hmask), mono);
-                send[bb] = tap(row, t, s_d[1], s_w[1], hmask);
+                mono = __fmaf_rn(__ldg(A.gain + s * kBands + bb), tap(row, t, d0, w0, hmask), mono);
+                send[bb] = tap(row, t, d1, w1, hmask);
             }
 #pragma unroll
-            for (int k = 0; k < kSh; ++k) bus[k] = __fmaf_rn(s_Y[k], mono, bus[k]);
+            for (int k = 0; k < kSh; ++k) bus[k] = __fmaf_rn(__ldg(A.Y + s * kSh + k), mono, bus[k]);
         }
         // stage `st` serves job j on its (j / kStages)-th use: phase parity
         mbar_wait(smem_addr(&s_full[st]), (uint32_t)(j / kStages) & 1u);
-        const float* sb = s_buf + (size_t)st * kLines * kWin;
+        const float* sb = s_buf + (size_t)st * kStageFloats;
+        const float* sM = sb + kStageM;
+        const float* sg = sb + kStageG;
         float y[kLines];
 #pragma unroll
         for (int i = 0; i < kLines; ++i) y[i] = sb[i * kWin + s_off[st][i] + n];
         float sum = 0.f;
 #pragma unroll
-        for (int i = 0; i < kLines; ++i) sum = __fmaf_rn(s_g[b * kLines + i], y[i], sum);
+        for (int i = 0; i < kLines; ++i) sum = __fmaf_rn(sg[i], y[i], sum);
         const float in = 0.25f * send[b] - (2.0f / kLines) * sum;   // Householder feedback
         float* ls = A.lines + ((size_t)s * kBands + b) * kLines * A.line_len;
         const int w = (int)(t & (A.line_len - 1));
 #pragma unroll
-        for (int i = 0; i < kLines; ++i) ls[(size_t)i * A.line_len + w] = __fmaf_rn(s_g[b * kLines + i], y[i], in);
+        for (int i = 0; i < kLines; ++i) ls[(size_t)i * A.line_len + w] = __fmaf_rn(sg[i], y[i], in);
         // line outputs -> SH bus through g_reverb,b * D_b * E
 #pragma unroll
         for (int k = 0; k < kSh; ++k) {
             float acc = bus[k];
 #pragma unroll
-            for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(s_M[(b * kSh + k) * kLines + i], y[i], acc);
+            for (int i = 0; i < kLines; ++i) acc = __fmaf_rn(sM[k * kLines + i], y[i], acc);
             bus[k] = acc;
         }
-        __syncthreads();   // stage st free for job j + kStages; parameters free after band 3
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&s_empty[st]));   // this warp is done with the stage
     }
     for (int k = 0; k < kSh; ++k) A.partial[((size_t)blockIdx.x * kSh + k) * kBlock + n] = bus[k];
 }
@@ -437,7 +449,7 @@ extern "C" int ef_audio_create(const ef_audio_config* cfg, const float* sos, con
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    A.grid = std::min(S, 2 * sms);   // two resident 512-thread CTAs per SM, persistent
+    A.grid = std::min(S, sms);   // one persistent 544-thread CTA per SM
     cudaError_t e = cudaSuccess;
 #define UP(f, src, n) if (e == cudaSuccess) e = up(&A.f, src, (size_t)(n), A.bytes);
     UP(sos, sos, kBands * kBiquads * 5);
@@ -494,7 +506,7 @@ extern "C" int ef_audio_process(ef_audio* h, const float* x, float* bus_out, flo
         if (e != cudaSuccess) return check_cuda(e, "render_kernel attributes");
         attr = true;
     }
-    render_kernel<<<A.grid, kBlock, kRenderDynSmem, st>>>(A);
+    render_kernel<<<A.grid, kRenderThreads, kRenderDynSmem, st>>>(A);
     reduce_kernel<<<kSh, kBlock, 0, st>>>(A, bus_out);
     bus_kernel<<<1, 512, 0, st>>>(A, out);
     count_launch(4);
