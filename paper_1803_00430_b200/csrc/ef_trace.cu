@@ -215,7 +215,6 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
 
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) {
-    constexpr int NK = (ORDER + 1) * (ORDER + 1);
     extern __shared__ __align__(16) unsigned char smem[];
     // per-block counters: f64 path-length sums, then u32 counters (a block's
     // per-source counts stay far below 2^32), then the all-pairs triangles
@@ -223,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     unsigned int* s_stats = reinterpret_cast<unsigned int*>(s_sumt + P.n_src);
     double* s_tri = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(s_stats + P.n_src * EF_ST_COUNT) + 15) & ~uintptr_t(15));
-    // traversal stacks (kSmemStack entries per thread), then the node cache
+    // traversal stacks (P.smem_stack entries per thread)
     uint2* s_stack = reinterpret_cast<uint2*>(
         (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0u;
