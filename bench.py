@@ -193,14 +193,15 @@ def run_reference(args, w, metric, unit):
     print(json.dumps(line), flush=True)
 
 
-def config_block(args, w, world):
+def config_block(args, w, world, exchange=None):
+    exchange = exchange or args.exchange
     return {"workload": f"{w.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c5': 4}[args.config] }])",
             "triangles": int(w.n_tri), "sources": int(len(w.sources)),
             "rays_per_source_per_rank": int(w.n_rays), "max_bounces": int(w.max_bounces),
             "sh_order": int(w.order), "bands": int(w.n_bands), "bins": int(w.n_bins),
             "parallelism": (f"rays sharded x{world}, " + (
                 "histograms reduce-scattered inside the trace kernel (ef_trace_fused, peer memory)"
-                if args.exchange == "fused" else "NCCL reduce-scatter of histograms")) if world > 1
+                if exchange == "fused" else "NCCL reduce-scatter of histograms")) if world > 1
             else "single GPU", "l2": "flushed between steps (256 MiB write)"}
 
 
@@ -235,12 +236,17 @@ def run_gpu(args, w, metric, unit):
     an = Analyzer(S_own, w.n_bins, sc.n_bands, w.order, w.bin_s)
     nk = cfg.n_coeffs
     fused = world > 1 and args.exchange == "fused"
+    exchange_note = None
     if fused:
-        from paper_1803_00430_b200.distributed import PeerHistograms
-        peers = PeerHistograms(S, w.n_bins, sc.n_bands, cfg.n_coeffs)
-        st_all = torch.empty_like(tr.stats)
-        su_all = torch.empty_like(tr.sum_t)
-    elif world > 1:
+        from paper_1803_00430_b200.distributed import PeerHistograms, PeerUnavailable
+        try:
+            peers = PeerHistograms(S, w.n_bins, sc.n_bands, cfg.n_coeffs)
+            st_all = torch.empty_like(tr.stats)
+            su_all = torch.empty_like(tr.sum_t)
+        except PeerUnavailable as e:   # every rank falls back together
+            fused = False
+            exchange_note = f"fused exchange unavailable ({e}); NCCL reduce-scatter used"
+    if world > 1 and not fused:
         H_own = torch.empty((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
         D_own = torch.empty((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
         st_own = torch.empty((S_own, tr.stats.shape[1]), dtype=torch.int64, device=dev)
@@ -394,7 +400,7 @@ def run_gpu(args, w, metric, unit):
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, w, world),
+            "config": config_block(args, w, world, "fused" if fused else "nccl"),
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps,
                     "host_enqueue_ms_per_step": host_enqueue_ms},
@@ -408,6 +414,8 @@ def run_gpu(args, w, metric, unit):
                                   (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))},
             "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
             "clocks": clocks.summary()}
+    if exchange_note:
+        line["exchange_note"] = exchange_note
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
         rays = max(1, int(w.n_rays * args.cpu_fraction))

@@ -85,6 +85,10 @@ class _CudaPeerBackend:
         _lib.torch().cuda.current_stream().synchronize()
 
 
+class PeerUnavailable(RuntimeError):
+    """Peer-mapped histogram blocks could not be set up on every rank."""
+
+
 class PeerHistograms:
     """This rank's share of the frame histograms, in peer-mapped memory.
 
@@ -120,27 +124,56 @@ class PeerHistograms:
         self._be = be
         nh = 4 * spr * n_bins * n_bands * nk
         nd = 4 * spr * n_bands * nk
-        self._own = [(be.alloc(nh), be.alloc(nd)) for _ in range(2)]   # [(ptr, handle)] per parity
-        mine = [(h[1], d[1]) for h, d in self._own]
+        # Every rank takes part in every collective below even when a local
+        # step fails, and the outcome is agreed on, so a rank that cannot map
+        # its peers (no CUDA IPC / P2P) makes ALL ranks raise PeerUnavailable
+        # together instead of leaving the others blocked in a collective.
+        self._own, self._opened, self._tab = [], [], []
+        err = None
+        try:
+            for _ in range(2):   # [(ptr, handle)] per parity
+                self._own.append((be.alloc(nh), be.alloc(nd)))
+            mine = [(h[1], d[1]) for h, d in self._own]
+        except Exception as e:   # noqa: BLE001 - reported to every rank below
+            err, mine = f"rank {self.rank}: peer allocation failed: {e}", None
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
-        self._opened = []
-        self._tab = []
-        for parity in range(2):
-            hp, dp = [], []
-            for r in range(self.world):
-                if r == self.rank:
-                    hp.append(self._own[parity][0][0])
-                    dp.append(self._own[parity][1][0])
-                else:
-                    ph = be.open(allh[r][parity][0])
-                    pd = be.open(allh[r][parity][1])
-                    self._opened += [ph, pd]
-                    hp.append(ph)
-                    dp.append(pd)
-            self._tab.append((be.table(hp), be.table(dp)))
+        if err is None and any(h is None for h in allh):
+            err = "a peer could not allocate its blocks"
+        if err is None:
+            try:
+                for parity in range(2):
+                    hp, dp = [], []
+                    for r in range(self.world):
+                        if r == self.rank:
+                            hp.append(self._own[parity][0][0])
+                            dp.append(self._own[parity][1][0])
+                        else:
+                            ph = be.open(allh[r][parity][0])
+                            self._opened.append(ph)
+                            pd = be.open(allh[r][parity][1])
+                            self._opened.append(pd)
+                            hp.append(ph)
+                            dp.append(pd)
+                    self._tab.append((be.table(hp), be.table(dp)))
+            except Exception as e:   # noqa: BLE001
+                err = f"rank {self.rank}: mapping a peer's blocks failed: {e}"
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [x for x in errs if x]
+        if bad:
+            self._release()
+            raise PeerUnavailable("; ".join(bad))
         self._H = [be.view(self._own[p][0][0], self.shape_h) for p in range(2)]
         self._D = [be.view(self._own[p][1][0], self.shape_d) for p in range(2)]
+
+    def _release(self):
+        for p in self._opened:
+            self._be.close(p)
+        for pair in self._own:
+            for ptr, _ in pair:
+                self._be.free(ptr)
+        self._own, self._opened = None, []
 
     def tables(self, frame: int):
         """(hist table, dir table) pointer arrays (one device pointer per rank)
@@ -169,13 +202,7 @@ class PeerHistograms:
             return
         self._be.sync()
         dist.barrier(group=self.group)        # no peer still writes into our blocks
-        for p in self._opened:
-            self._be.close(p)
-        for (ph, _), (pd, _) in self._own:
-            self._be.free(ph)
-            self._be.free(pd)
-        self._own = None
-        self._opened = []
+        self._release()
 
 
 class EmulatedPeers:

@@ -186,3 +186,46 @@ def test_peer_histograms_protocol(tmp_path):
             blk = res[g // 2][frame][g % 2]
             scale = np.abs(r.H).max()
             np.testing.assert_allclose(blk, r.H, rtol=1e-5, atol=1e-6 * scale)
+
+
+class _FailingOpenBackend(_ShmBackend):
+    """Rank 1 cannot map its peer's blocks (no IPC / P2P on this node)."""
+
+    def open(self, handle):
+        if self.rank == 1:
+            raise OSError("cudaIpcOpenMemHandle: peer access not supported")
+        return super().open(handle)
+
+
+def _unavailable_worker(rank, world, port, tmpdir, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1803_00430_b200 import distributed
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        distributed.PeerHistograms(4, 16, 4, 16, backend=_FailingOpenBackend(tmpdir, rank))
+        q.put((rank, "no error"))
+    except distributed.PeerUnavailable as e:
+        q.put((rank, "unavailable: " + str(e)))
+    dist.barrier()                 # both ranks got here: nobody hangs in a collective
+    dist.destroy_process_group()
+
+
+def test_peer_setup_failure_is_agreed_by_every_rank(tmp_path):
+    """One rank failing to map its peers makes every rank raise
+    PeerUnavailable (bench.py then falls back to the NCCL exchange), instead
+    of leaving the others blocked in a collective."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unavailable_worker, args=(r, world, port, str(tmp_path), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(v.startswith("unavailable") and "rank 1" in v for v in res.values()), res
