@@ -17,6 +17,10 @@
  *     message of the last failure on the calling thread is available through
  *     ef_last_error().  Contract violations -> EF_EINVAL (Python: ValueError),
  *     CUDA failures -> EF_ECUDA (Python: RuntimeError).
+ *   - Stream-ordered scratch comes from the device's default memory pool
+ *     (cudaMallocAsync); the library sets that pool's release threshold to
+ *     "keep everything" so per-frame scratch is not re-mapped at every
+ *     synchronisation.
  *   - ef_scene handles are immutable after ef_scene_create and may be used
  *     concurrently from several streams.
  */

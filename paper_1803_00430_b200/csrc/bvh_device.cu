@@ -105,21 +105,31 @@ __global__ void prim_box_kernel(const double* __restrict__ v0, const double* __r
 
 __global__ void morton_kernel(const double* __restrict__ pbox, int64_t n, const BuildBounds* bb,
                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-    float lo[3], inv[3];
+    // cubic cells (one scale for all axes, the largest centroid extent):
+    // flat scenes such as cities then split along their long axes first
+    float lo[3], inv[3], ext = 0.0f;
     for (int k = 0; k < 3; ++k) {
         lo[k] = o2f(bb->cmin[k]);
-        const float ext = o2f(bb->cmax[k]) - lo[k];
-        inv[k] = ext > 0.0f ? 2097151.0f / ext : 0.0f;
+        ext = fmaxf(ext, o2f(bb->cmax[k]) - lo[k]);
     }
+    for (int k = 0; k < 3; ++k) inv[k] = ext > 0.0f ? 2097151.0f / ext : 0.0f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t key = 0;
+        float diag2 = 0.0f;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float c = (float)(0.5 * (pbox[6 * i + k] + pbox[6 * i + 3 + k]));
             const float q = fminf(fmaxf((c - lo[k]) * inv[k], 0.0f), 2097151.0f);
             key |= spread21((uint32_t)q) << (2 - k);
+            const float e = (float)(pbox[6 * i + 3 + k] - pbox[6 * i + k]);
+            diag2 += e * e;
         }
+        // triangles spanning a quarter of the scene (ground planes, long
+        // walls) sort after all others: the hierarchy splits them off at the
+        // root instead of inflating the boxes of small-triangle subtrees
+        key >>= 1;   // 62 Morton bits under the flag: a 63-bit sort
+        if (diag2 > 0.0625f * ext * ext) key |= 1ull << 62;
         keys[i] = key;
         vals[i] = (uint32_t)i;
     }
@@ -339,6 +349,7 @@ int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const doub
     if (n64 <= 0) return EF_OK;
     if (n64 >= (1ll << 29)) return set_error(EF_EUNSUPPORTED, "device BVH build: more than 2^29 triangles");
     const int n = (int)n64;
+    keep_pool_memory();
     const int max_leaf = kMaxLeaf;
     const int64_t cap = n64;   // each four-child node comes from a distinct binary inner node
 

@@ -390,6 +390,7 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
     if (!(cfg->bin_s > 0.0) || !(cfg->max_rt >= 0.05)) return set_error(EF_EINVAL, "ef_analyze: bad bin_s / max_rt");
     cudaStream_t st = (cudaStream_t)stream;
     int* counters = nullptr;
+    keep_pool_memory();
     cudaError_t e = cudaMallocAsync((void**)&counters, sizeof(int) * cfg->n_sources, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, sizeof(int) * cfg->n_sources, st);
     if (e != cudaSuccess) return check_cuda(e, "ef_analyze scratch");

@@ -22,6 +22,22 @@ int check_cuda(int err, const char* what) {
     return set_error(EF_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)err));
 }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Stream-ordered scratch (cudaMallocAsync: the trace counter, the analysis
+// counters, the BVH builder's temporaries) comes from the device's default
+// pool.  Keep what the pool holds instead of returning it to the driver at
+// every synchronisation, so per-frame allocations do not re-map memory.
+void keep_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
 }  // namespace ef
 
 extern "C" int ef_abi_version(void) { return EF_ABI_VERSION; }

@@ -100,4 +100,5 @@ namespace ef {
 int set_error(int code, const std::string& msg);
 int check_cuda(int err, const char* what);
 void count_launch(uint64_t n = 1);
+void keep_pool_memory();   // default mempool keeps its memory (cudaMallocAsync scratch)
 }  // namespace ef

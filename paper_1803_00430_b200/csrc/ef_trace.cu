@@ -705,6 +705,7 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
     }
     unsigned long long* counter = nullptr;
+    keep_pool_memory();
     e = cudaMallocAsync((void**)&counter, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return check_cuda(e, "cudaMallocAsync");
     for (int s0 = 0; s0 < cfg->n_sources; s0 += kMaxSourcesPerLaunch) {
