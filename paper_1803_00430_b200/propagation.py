@@ -142,10 +142,72 @@ def build_path_list(entries: np.ndarray, n_bands: int, speed_of_sound: float,
 
 @dataclass
 class CoherenceCaches:
-    """Temporal IR cache: exponentially smoothed histograms
-    per source key, updated by ``accumulate_ir``."""
+    """Temporal coherence caches.
+
+    * ``ir``: per source key, the exponentially smoothed LowRateIR
+      (accumulate_ir, tau_LR = 3 s).
+    * ``er``: the diffuse path cache -- per reflection sequence (source,
+      order, first two triangles), exponentially smoothed per-band energies,
+      SH directivity and delay (tau_ER = 1 s).  A sequence missing from a
+      frame decays with the same blend (its frame contribution is zero).
+    * entries not refreshed for 2 tau expire (``clock`` is the time of the
+      latest update)."""
     tau_lr: float = TAU_LR
+    tau_er: float = TAU_ER
     ir: dict = field(default_factory=dict)
+    er: dict = field(default_factory=dict)
+    ir_seen: dict = field(default_factory=dict)
+    clock: float = 0.0
+
+    def update_er(self, paths: "PathList", dt: float) -> "PathList":
+        """Fold one frame's PathList into the diffuse path cache; returns the
+        cached paths (ER go to the PathList via this cache)."""
+        if dt <= 0:
+            raise ValueError("dt must be > 0")
+        self.clock += dt
+        a = 1.0 - math.exp(-dt / self.tau_er) if self.tau_er > 0 else 1.0
+        fresh = {}
+        for j in range(len(paths)):
+            k = (int(paths.sources[j]), int(paths.orders[j]), int(paths.triangles[j][0]),
+                 int(paths.triangles[j][1]))
+            fresh[k] = (paths.pressures[j] ** 2, paths.directivities[j], float(paths.delays[j]))
+        nb = paths.pressures.shape[1] if len(paths) else (
+            next(iter(self.er.values()))["energy"].shape[0] if self.er else 4)
+        for k in set(self.er) | set(fresh):
+            e_new, y_new, d_new = fresh.get(k, (np.zeros(nb), np.zeros(9), None))
+            c = self.er.get(k)
+            if c is None:
+                self.er[k] = {"energy": np.array(e_new, float), "dir": np.array(y_new, float),
+                              "delay": d_new, "seen": self.clock}
+                continue
+            c["energy"] = a * np.asarray(e_new, float) + (1.0 - a) * c["energy"]
+            c["dir"] = a * np.asarray(y_new, float) + (1.0 - a) * c["dir"]
+            if d_new is not None:
+                c["delay"] = d_new
+                c["seen"] = self.clock
+        self.expire()
+        keys = sorted(self.er)
+        if not keys:
+            return PathList(pressures=np.zeros((0, nb)), dropped=paths.dropped)
+        E = np.stack([self.er[k]["energy"] for k in keys])
+        return PathList(delays=np.array([self.er[k]["delay"] for k in keys]),
+                        pressures=np.sqrt(E), directivities=np.stack([self.er[k]["dir"] for k in keys]),
+                        kinds=["early-reflection"] * len(keys),
+                        sources=np.array([k[0] for k in keys], np.int64),
+                        orders=np.array([k[1] for k in keys], np.int64),
+                        triangles=np.array([[k[2], k[3]] for k in keys], np.int64),
+                        dropped=paths.dropped)
+
+    def touch_ir(self, key):
+        self.ir_seen[key] = self.clock
+
+    def expire(self):
+        """Drop entries not refreshed for 2 tau."""
+        for k in [k for k, c in self.er.items() if self.clock - c["seen"] > 2.0 * self.tau_er]:
+            del self.er[k]
+        for k in [k for k, t in self.ir_seen.items() if self.clock - t > 2.0 * self.tau_lr]:
+            self.ir.pop(k, None)
+            del self.ir_seen[k]
 
 
 def _stats_from_row(row: np.ndarray, sum_t: float) -> TraceStats:
@@ -292,8 +354,9 @@ def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceC
 
     ``rng``: an int seed (overrides config.seed) or None.  Returns
     (PathList, LowRateIR, TraceStats).  With ``caches`` and ``dt`` the IR is
-    folded into the temporal cache (accumulate_ir) and the cached IR is
-    returned (SPEC.md:210, 225-233)."""
+    folded into the temporal IR cache (accumulate_ir) and the early
+    reflections into the diffuse path cache, and the cached versions are
+    returned (SPEC.md:201-204, 210, 225-233)."""
     if config.primary_rays < 1 or config.max_order < 1:
         raise ValueError("config.primary_rays and config.max_order must be >= 1")
     seed = config.seed if rng is None else int(rng)
@@ -313,10 +376,16 @@ def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceC
     tr.set_sources(np.asarray(pos)[None, :], [key])
     tr.trace(lpos, frame=frame)
     ir = tr.irs()[0]
+    paths = tr.path_list() if cfg.er_max_order > 0 else PathList()
     if caches is not None and dt is not None:
         ir = accumulate_ir(caches.ir.get(key), ir, caches.tau_lr, dt)
         caches.ir[key] = ir
-    paths = tr.path_list() if cfg.er_max_order > 0 else PathList()
+        if cfg.er_max_order > 0:
+            paths = caches.update_er(paths, dt)      # advances the cache clock
+        else:
+            caches.clock += dt
+            caches.expire()
+        caches.touch_ir(key)
     return paths, ir, tr.trace_stats()[0]
 
 

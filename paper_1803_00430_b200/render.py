@@ -123,3 +123,33 @@ class SHRenderer:
         if h is not None and _lib._lib is not None:
             _lib._lib.ef_audio_destroy(h)
             self._h = None
+
+
+THRESHOLD_OF_HEARING = 1e-12   # W/m^2
+N_ER = 100                     # rendered early reflections (§5)
+
+
+def prioritize_paths(paths, threshold: float = THRESHOLD_OF_HEARING, max_paths: int = N_ER):
+    """render_early's path selection: drop paths whose
+    intensity (sum over bands of pressure^2) is below the threshold of
+    hearing, sort the rest by decreasing intensity (stable: equal intensities
+    keep their order) and keep the first ``max_paths`` across all sources.
+    Returns (kept PathList, dropped PathList) -- the dropped reflection paths
+    go back to the IR for reinjection."""
+    from .propagation import PathList
+    P = np.asarray(paths.pressures, np.float64)
+    inten = (P ** 2).sum(axis=1) if len(paths) else np.zeros(0)
+    audible = np.nonzero(inten >= threshold)[0]
+    order = audible[np.argsort(-inten[audible], kind="stable")]
+    keep, drop = order[:max_paths], np.setdiff1d(np.arange(len(paths)), order[:max_paths])
+
+    def take(idx):
+        return PathList(delays=np.asarray(paths.delays)[idx], pressures=P[idx],
+                        directivities=np.asarray(paths.directivities)[idx],
+                        kinds=[paths.kinds[i] for i in idx],
+                        sources=np.asarray(paths.sources)[idx] if len(paths.sources) else paths.sources,
+                        orders=np.asarray(paths.orders)[idx] if len(paths.orders) else paths.orders,
+                        triangles=np.asarray(paths.triangles)[idx] if len(paths.triangles) else paths.triangles)
+    kept, dropped = take(keep), take(drop)
+    kept.dropped = len(drop)
+    return kept, dropped
