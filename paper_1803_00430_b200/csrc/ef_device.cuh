@@ -66,27 +66,36 @@ __device__ __forceinline__ void sample_sphere(uint32_t seed, uint32_t src, uint3
     }
 }
 
-// Cosine lobe about unit n: disk rejection + Duff et al. ONB.
+// Direction of an accepted disk point (a, b), s = a^2 + b^2 < 1, lifted to
+// the cosine lobe about unit n with the Duff et al. ONB.
+__device__ __forceinline__ void cosine_dir(double a, double b, double s, double nx, double ny,
+                                           double nz, double& dx, double& dy, double& dz) {
+    const double z = sqrt(1.0 - s);
+    const double sg = copysign(1.0, nz);
+    const double aa = -1.0 / (sg + nz);
+    const double bb = nx * ny * aa;
+    const double t1x = 1.0 + sg * nx * nx * aa, t1y = sg * bb, t1z = -sg * nx;
+    const double t2x = bb, t2y = sg + ny * ny * aa, t2z = -ny;
+    dx = (a * t1x + b * t2x) + z * nx;
+    dy = (a * t1y + b * t2y) + z * ny;
+    dz = (a * t1z + b * t2z) + z * nz;
+}
+
+// Cosine lobe about unit n: disk rejection (candidate j from draw 1 + j,
+// starting at candidate j0) + cosine_dir.
 __device__ __forceinline__ void sample_cosine(uint32_t seed, uint32_t src, uint32_t ray,
                                               uint32_t bounce, uint32_t frame, double nx, double ny,
-                                              double nz, double& dx, double& dy, double& dz) {
+                                              double nz, double& dx, double& dy, double& dz,
+                                              uint32_t j0 = 0) {
     dx = nx; dy = ny; dz = nz;
-    for (uint32_t j = 0; j < 64u; ++j) {
+    for (uint32_t j = j0; j < 64u; ++j) {
         double u1, u2;
         draw2(ray, bounce, 1u + j, frame, seed, src, u1, u2);
         const double a = 2.0 * u1 - 1.0;
         const double b = 2.0 * u2 - 1.0;
         const double s = a * a + b * b;
         if (s >= 1.0) continue;
-        const double z = sqrt(1.0 - s);
-        const double sg = copysign(1.0, nz);
-        const double aa = -1.0 / (sg + nz);
-        const double bb = nx * ny * aa;
-        const double t1x = 1.0 + sg * nx * nx * aa, t1y = sg * bb, t1z = -sg * nx;
-        const double t2x = bb, t2y = sg + ny * ny * aa, t2z = -ny;
-        dx = (a * t1x + b * t2x) + z * nx;
-        dy = (a * t1y + b * t2y) + z * ny;
-        dz = (a * t1z + b * t2z) + z * nz;
+        cosine_dir(a, b, s, nx, ny, nz, dx, dy, dz);
         break;
     }
 }
@@ -360,6 +369,35 @@ struct TravStackMem {
     __device__ __forceinline__ uint2 top() const { return sp < depth ? s[sp * stride] : l[sp]; }
 };
 
+// The whole stack in shared memory (the host guarantees depth >= the tree's
+// max_stack): pushes are predicated stores, no overflow branch.
+struct TravStackShared {
+    uint32_t sbase;
+    uint32_t sstep;
+    int sp;
+
+    // push `node, key` if `valid` (no branch: predicated st.shared)
+    __device__ __forceinline__ void push_if(int32_t node, uint32_t key, bool valid) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+            "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(sbase + (uint32_t)sp * sstep),
+            "r"((uint32_t)node), "r"(key), "r"((uint32_t)valid));
+        sp += valid ? 1 : 0;
+    }
+    __device__ __forceinline__ uint2 top() const {
+        uint2 e;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
+                     : "r"(sbase + (uint32_t)sp * sstep));
+        return e;
+    }
+};
+
+__device__ __forceinline__ void init_stack(TravStackShared& st, uint2*, uint2* s_stack, int) {
+    st.sbase = (uint32_t)__cvta_generic_to_shared(s_stack);
+    st.sstep = 8u * blockDim.x;
+    st.sp = 0;
+}
+
 __device__ __forceinline__ void init_stack(TravStack& st, uint2* overflow, uint2* s_stack,
                                            int s_depth) {
     st.l = overflow;
@@ -384,7 +422,7 @@ __device__ __forceinline__ void init_stack(TravStackMem& st, uint2*, uint2* s_st
 // selects the forms measured faster in the 512-thread kernel (slab_key_minmax,
 // the register-resident TravStack) over those of the register-starved
 // 768-thread one (slab_key, TravStackMem).
-template <bool MINMAX = true>
+template <bool MINMAX = true, bool SSTACK = false>
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
@@ -395,8 +433,9 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
-    uint2 overflow[kStackSize];   // TravStack's local overflow (unused by TravStackMem)
-    typename std::conditional<MINMAX, TravStack, TravStackMem>::type st;
+    uint2 overflow[SSTACK ? 1 : kStackSize];   // TravStack's local overflow
+    typename std::conditional<SSTACK, TravStackShared,
+                              typename std::conditional<MINMAX, TravStack, TravStackMem>::type>::type st;
     init_stack(st, overflow, s_stack, s_depth);
     int32_t node = 0;
     bool done = false;
@@ -430,9 +469,15 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
-            if (k3 != 0xffffffffu) st.push(pick(ch, k3 & 3u), k3);
-            if (k2 != 0xffffffffu) st.push(pick(ch, k2 & 3u), k2);
-            if (k1 != 0xffffffffu) st.push(pick(ch, k1 & 3u), k1);
+            if constexpr (SSTACK) {
+                st.push_if(pick(ch, k3 & 3u), k3, k3 != 0xffffffffu);
+                st.push_if(pick(ch, k2 & 3u), k2, k2 != 0xffffffffu);
+                st.push_if(pick(ch, k1 & 3u), k1, k1 != 0xffffffffu);
+            } else {
+                if (k3 != 0xffffffffu) st.push(pick(ch, k3 & 3u), k3);
+                if (k2 != 0xffffffffu) st.push(pick(ch, k2 & 3u), k2);
+                if (k1 != 0xffffffffu) st.push(pick(ch, k1 & 3u), k1);
+            }
             if (k0 != 0xffffffffu) {
                 node = pick(ch, k0 & 3u);
                 EF_PHASE_ADD(0, tv);

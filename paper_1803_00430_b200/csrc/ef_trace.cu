@@ -42,6 +42,7 @@ static int smem_stack_depth_host() {
 // the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
 // removed; profiles/r01_node_cache_sweep.txt.)
 constexpr size_t kMaxTraceSmem = 220 * 1024;
+constexpr size_t kMaxSstackBytes = 128 * 1024;   // leave >= 128 KB of the SM's 256 KB to L1
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr int kMaxRanks = 8;   // GPUs of one node reachable by ef_trace_fused
 constexpr unsigned kFull = 0xffffffffu;
@@ -76,6 +77,36 @@ __device__ __forceinline__ Hit closest_brute(const double* __restrict__ s_tri, i
         if (mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, t_max, t) && t < h.t) {
             h.t = t;
             h.id = i;
+        }
+    }
+    return h;
+}
+
+// All-pairs closest hit shared by the G lanes of a lane group (G a power of
+// two dividing 32, `gmask` the group's lanes, `gl` this lane's rank in it):
+// lane gl tests triangles gl, gl+G, ... against t_max alone, then a
+// butterfly over the group keeps the lexicographic minimum of (t, id) -- the
+// same answer as closest_brute (lowest id on equal t), on every lane.
+template <int G>
+__device__ __forceinline__ Hit closest_brute_group(const double* __restrict__ s_tri, int n, double ox,
+                                                   double oy, double oz, double dx, double dy,
+                                                   double dz, double t_min, double t_max,
+                                                   unsigned gmask, int gl) {
+    Hit h{INFINITY, INT32_MAX};
+    for (int i = gl; i < n; i += G) {
+        double t;
+        if (mt_hit(ox, oy, oz, dx, dy, dz, s_tri + 9 * i, t_min, t_max, t) && t < h.t) {
+            h.t = t;
+            h.id = i;
+        }
+    }
+#pragma unroll
+    for (int k = G / 2; k >= 1; k >>= 1) {
+        const double t2 = __shfl_xor_sync(gmask, h.t, k, G);
+        const int id2 = __shfl_xor_sync(gmask, h.id, k, G);
+        if (t2 < h.t || (t2 == h.t && id2 < h.id)) {
+            h.t = t2;
+            h.id = id2;
         }
     }
     return h;
@@ -213,8 +244,16 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
     }
 }
 
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
+// G > 1 (all-pairs scenes with few paths, C1): G lanes share one path, split
+// its triangle tests (closest_brute_group) and otherwise run identical,
+// deterministic path code; the group's first lane alone commits arrivals,
+// counters and records.
+// SSTACK: the whole traversal stack in shared memory (P.smem_stack >= the
+// tree's max_stack), predicated pushes.
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
 __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) {
+    static_assert(G == 1 || BRUTE, "lane groups are for the all-pairs path");
+    static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
     extern __shared__ __align__(16) unsigned char smem[];
     // per-block counters: f64 path-length sums, then u32 counters (a block's
     // per-source counts stay far below 2^32), then the all-pairs triangles
@@ -232,6 +271,10 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);                 // rank in the lane group
+    const int gbase = lane - gl;
+    const unsigned gmask = G == 32 ? kFull : ((1u << G) - 1u) << gbase;
+    const bool lead = gl == 0;
     const int nb = P.nb;
     LaneStats ls;
     bool active = false, exhausted = false;
@@ -248,15 +291,17 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
 
     for (;;) {
         // ---- warp-aggregated refill: idle lanes take the next path indices
+        // (lane groups: only group leads count; a group's lanes share its
+        // lead's path index)
         const bool need = !active && !exhausted;
-        const unsigned mask = __ballot_sync(kFull, need);
+        const unsigned mask = __ballot_sync(kFull, need && lead);
         if (mask) {
             const int leader = __ffs(mask) - 1;
             unsigned long long base = 0;
             if (lane == leader) base = atomicAdd(P.counter, (unsigned long long)__popc(mask));
             base = __shfl_sync(kFull, base, leader);
             if (need) {
-                path = base + __popc(mask & ((1u << lane) - 1u));
+                path = base + __popc(mask & ((1u << gbase) - 1u));
                 if (path >= P.total) {
                     exhausted = true;
                 } else {
@@ -276,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                     tri0 = tri1 = -1;
                     last_diffuse = false;
                     if (src != ls.src) {
-                        flush_stats(ls, s_stats, s_sumt);
+                        if (lead) flush_stats(ls, s_stats, s_sumt);   // other group lanes' counts are dropped
                         ls.src = src;
                     }
                     ls.c[EF_ST_PATHS]++;
@@ -291,16 +336,20 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         // ---- closest hit (exact f64 leaf test)
         Hit h;
         if (BRUTE) {
-            h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
+            if (G > 1)
+                h = closest_brute_group<G>(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY,
+                                           gmask, gl);
+            else
+                h = closest_brute(s_tri, P.n_tri, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY);
             ls.c[EF_ST_TRIS] += P.n_tri;
         }
         else
-            h = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY,
+            h = closest_bvh<(THREADS <= 512), SSTACK>(P.nodes, P.tris, ox, oy, oz, dx, dy, dz, kRayEps, INFINITY,
                             ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
                             s_stack + threadIdx.x, P.smem_stack);
         const bool hit = h.id != INT32_MAX;
         EF_PHASE_T0(tsh);
-        if (P.path_ids && !P.timing) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
+        if (P.path_ids && !P.timing && lead) P.path_ids[path * P.max_bounces + nseg] = hit ? h.id : -1;
 
         // ---- listener sphere receiver + SH histogram commit (with diffuse
         // rain, segments leaving a diffuse bounce reach the listener only
@@ -312,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             if (tc > 0.0 && tc < tlim) {
                 const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
                 const double perp2 = dist2 - tc * tc;
-                if (perp2 <= P.r2)
+                if (perp2 <= P.r2 && lead)
                     commit_arrival<NBMAX, ORDER>(P, src, nrefl, tri0, tri1, plen + tc, -dx, -dy, -dz,
                                                  E, ls);
             }
@@ -339,7 +388,15 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             const double ny = __ldg(P.normals + 3 * h.id + 1);
             const double nz = __ldg(P.normals + 3 * h.id + 2);
             double u1, u2;
-            draw2(ray, (uint32_t)nrefl, 0u, P.frame, P.seed, skey, u1, u2);
+            uint4 xg;   // lane groups: this lane's draw (ray, bounce, gl) -- all of a
+                        // group's draws come from one Philox latency instead of a chain
+            if (G > 1) {
+                xg = philox(make_uint4(ray, (uint32_t)nrefl, (uint32_t)gl, P.frame),
+                            make_uint2(P.seed, skey));
+                u1 = u53(__shfl_sync(gmask, xg.x, 0, G), __shfl_sync(gmask, xg.y, 0, G));
+            } else {
+                draw2(ray, (uint32_t)nrefl, 0u, P.frame, P.seed, skey, u1, u2);
+            }
             const bool diffuse = u1 < __ldg(P.pdiff + m);
             const double nd = dot3(nx, ny, nz, dx, dy, dz);
             if (P.rain && diffuse) {
@@ -356,13 +413,17 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                     const double limit = dd - kRayEps;
                     Hit sh;
                     if (BRUTE) {
-                        sh = closest_brute(s_tri, P.n_tri, ox, oy, oz, ex, ey, ez, kRayEps, limit);
+                        if (G > 1)
+                            sh = closest_brute_group<G>(s_tri, P.n_tri, ox, oy, oz, ex, ey, ez, kRayEps,
+                                                        limit, gmask, gl);
+                        else
+                            sh = closest_brute(s_tri, P.n_tri, ox, oy, oz, ex, ey, ez, kRayEps, limit);
                     } else {
-                        sh = closest_bvh<(THREADS <= 512)>(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit,
+                        sh = closest_bvh<(THREADS <= 512), SSTACK>(P.nodes, P.tris, ox, oy, oz, ex, ey, ez, kRayEps, limit,
                                          ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS],
                                          s_stack + threadIdx.x, P.smem_stack, true);
                     }
-                    if (sh.id == INT32_MAX) {
+                    if (sh.id == INT32_MAX && lead) {
                         const float gf = (float)(cosv * P.r2 / d2);
                         float c[NBMAX];
 #pragma unroll
@@ -380,8 +441,25 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
                 if (b < nb) E[b] = E[b] * __ldg(f + b);
             if (diffuse) {
                 const double s = nd > 0.0 ? -1.0 : 1.0;
-                sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny, s * nz,
-                              dx, dy, dz);
+                if (G > 1) {
+                    // disk candidate j = gl - 1 on lanes 1..G-1; the first accepted
+                    // one (lowest j) is the sequential loop's answer
+                    const double a = 2.0 * u53(xg.x, xg.y) - 1.0;
+                    const double b = 2.0 * u53(xg.z, xg.w) - 1.0;
+                    const double ss = a * a + b * b;
+                    const unsigned ok = __ballot_sync(gmask, gl >= 1 && ss < 1.0);
+                    if (ok) {
+                        const int f = __ffs(ok) - 1 - gbase;
+                        cosine_dir(__shfl_sync(gmask, a, f, G), __shfl_sync(gmask, b, f, G),
+                                   __shfl_sync(gmask, ss, f, G), s * nx, s * ny, s * nz, dx, dy, dz);
+                    } else {
+                        sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny,
+                                      s * nz, dx, dy, dz, (uint32_t)(G - 1));
+                    }
+                } else {
+                    sample_cosine(P.seed, skey, ray, (uint32_t)nrefl, P.frame, s * nx, s * ny, s * nz,
+                                  dx, dy, dz);
+                }
             } else {
                 const double k2 = 2.0 * nd;
                 dx = dx - k2 * nx;
@@ -394,8 +472,10 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
 #ifdef EF_PROFILE_PHASES
         atomicAdd(&g_phase[4], 1ull);
 #endif
-        if (!active && P.path_nseg) P.path_nseg[path] = nseg;
-        if (!active && P.timing) {
+        if (!active && P.path_nseg && lead) P.path_nseg[path] = nseg;
+        if (P.timing && lead && 5 + nseg < P.max_bounces)   // debug: ns since path start, per segment
+            P.path_ids[path * P.max_bounces + 5 + nseg] = (int32_t)(globaltimer() - t_start);
+        if (!active && P.timing && lead) {
             const unsigned long long t_end = globaltimer();
             int32_t* row = P.path_ids + path * P.max_bounces;
             unsigned smid;
@@ -408,7 +488,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             row[5] = nseg;
         }
     }
-    flush_stats(ls, s_stats, s_sumt);
+    if (lead) flush_stats(ls, s_stats, s_sumt);
     __syncthreads();
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x)
         if (s_stats[i]) atomicAdd(P.stats + i, (unsigned long long)s_stats[i]);
@@ -427,22 +507,23 @@ static int sm_count() {
     return n;
 }
 
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
 static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     TraceParams P = P0;
-    P.smem_stack = smem_stack_depth_host<THREADS>();
+    if (!SSTACK) P.smem_stack = smem_stack_depth_host<THREADS>();   // else: the tree's max_stack
     // Too few paths to give every SM a full CTA (C1: 4,096 paths): spread them
     // over all SMs in smaller CTAs (>= one warp), so each path's latency-bound
     // chain shares its SM with as few others as possible.
     const long long sms = (long long)sm_count();
+    const long long lanes = (long long)P.total * G;
     int block = THREADS;
-    if ((long long)P.total < sms * THREADS) {
-        const long long per = ((long long)P.total + sms - 1) / sms;
+    if (lanes < sms * THREADS) {
+        const long long per = (lanes + sms - 1) / sms;
         block = (int)std::min<long long>(THREADS, std::max<long long>(32, (per + 31) / 32 * 32));
     }
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
                   (BRUTE ? 0 : (size_t)P.smem_stack * block * sizeof(uint2));
-    auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS>;
+    auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -453,28 +534,53 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     if (smem > kMaxTraceSmem) return cudaErrorInvalidValue;
     // persistent grid: one CTA per SM (__launch_bounds__(THREADS, 1) and the
     // register budget leave room for exactly one), no more warps than paths
-    const long long need = ((long long)P.total + block - 1) / block;
+    const long long need = (lanes + block - 1) / block;
     const int grid = (int)std::max(1LL, std::min(sms, need));
     kern<<<grid, block, smem, st>>>(P);
     count_launch();
     return cudaGetLastError();
 }
 
-template <int NBMAX, bool BRUTE, int THREADS>
+template <int NBMAX, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
 static cudaError_t dispatch_order(int order, const TraceParams& P, cudaStream_t st) {
     switch (order) {
-        case 0: return launch_trace<NBMAX, 0, BRUTE, THREADS>(P, st);
-        case 1: return launch_trace<NBMAX, 1, BRUTE, THREADS>(P, st);
-        case 2: return launch_trace<NBMAX, 2, BRUTE, THREADS>(P, st);
-        case 3: return launch_trace<NBMAX, 3, BRUTE, THREADS>(P, st);
-        default: return launch_trace<NBMAX, 4, BRUTE, THREADS>(P, st);
+        case 0: return launch_trace<NBMAX, 0, BRUTE, THREADS, G, SSTACK>(P, st);
+        case 1: return launch_trace<NBMAX, 1, BRUTE, THREADS, G, SSTACK>(P, st);
+        case 2: return launch_trace<NBMAX, 2, BRUTE, THREADS, G, SSTACK>(P, st);
+        case 3: return launch_trace<NBMAX, 3, BRUTE, THREADS, G, SSTACK>(P, st);
+        default: return launch_trace<NBMAX, 4, BRUTE, THREADS, G, SSTACK>(P, st);
     }
+}
+
+// Lanes per path on the all-pairs path: the widest group (<= the triangle
+// count rounded up to a power of two, <= 16) whose lanes still fit one full
+// CTA per SM, so a frame with few paths (C1: 4,096) spreads each path's
+// triangle tests over idle lanes instead of leaving SMs empty.  EF_GROUP
+// (1, 4, 8, 16) overrides (tuning).
+static int brute_group(unsigned long long paths, int n_tri) {
+    static const int force = [] {
+        const char* e = std::getenv("EF_GROUP");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (force == 1 || force == 4 || force == 8 || force == 16) return force;
+    const unsigned long long cap = (unsigned long long)sm_count() * kSmallThreads;
+    int g = 16;
+    while (g > 1 && ((unsigned long long)g * paths > cap || g / 2 >= n_tri)) g /= 2;
+    return g == 2 ? 1 : g;   // no 2-lane instantiation
 }
 
 template <int NBMAX>
 static cudaError_t dispatch(bool brute, bool big, int order, const TraceParams& P, cudaStream_t st) {
-    if (brute) return dispatch_order<NBMAX, true, kSmallThreads>(order, P, st);
+    if (brute) {
+        switch (brute_group(P.total, P.n_tri)) {
+            case 16: return dispatch_order<NBMAX, true, kSmallThreads, 16>(order, P, st);
+            case 8: return dispatch_order<NBMAX, true, kSmallThreads, 8>(order, P, st);
+            case 4: return dispatch_order<NBMAX, true, kSmallThreads, 4>(order, P, st);
+            default: return dispatch_order<NBMAX, true, kSmallThreads>(order, P, st);
+        }
+    }
     if (big) return dispatch_order<NBMAX, false, kBigThreads>(order, P, st);
+    if (P.smem_stack > 0) return dispatch_order<NBMAX, false, kSmallThreads, 1, true>(order, P, st);
     return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
 }
 
@@ -773,6 +879,17 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         const bool big = force_big >= 0 ? force_big == 1
                                          : (int64_t)s->n_nodes * (int64_t)sizeof(GpuNode) +
                                                    s->n_refs * (int64_t)sizeof(GpuTri) > kBigSceneBytes;
+        // the whole traversal stack in shared memory when the tree's bound
+        // fits next to the counters (EF_SSTACK=0 disables; tuning)
+        static const int sstack_env = [] {
+            const char* e = std::getenv("EF_SSTACK");
+            return e ? std::atoi(e) : 1;
+        }();
+        const int max_stack = 3 * s->max_depth + 1;
+        const size_t sstack_bytes = (size_t)max_stack * kSmallThreads * sizeof(uint2) +
+                                    (size_t)ns * (EF_ST_COUNT * 4 + 8) + 64;
+        P.smem_stack = (!brute && !big && sstack_env && max_stack <= kStackSize &&
+                        sstack_bytes <= kMaxSstackBytes) ? max_stack : 0;
         if (s->n_bands <= 4)
             e = dispatch<4>(brute, big, cfg->order, P, st);
         else

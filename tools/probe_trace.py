@@ -82,6 +82,11 @@ def timing(name="c2"):
     for i in order:
         print(f"  path {i}: start {t0[i]:.1f} end {t1[i]:.1f} dur {dur[i]:.1f} us nseg {nseg[i]} "
               f"({dur[i] / max(nseg[i], 1):.2f} us/seg) sm {rows[i, 4]}")
+    full = tr.path_ids.cpu().numpy().reshape(-1, w.max_bounces)
+    i = int(np.argmax(t1))
+    seg_t = full[i, 6:6 + min(nseg[i], w.max_bounces - 6)] / 1e3 + t0[i]
+    print("  longest path: absolute end time (us) of segments 1..:",
+          " ".join(f"{x:.0f}" for x in seg_t[::5]), "(every 5th)")
     for k in (1, 2, 4, 10, 50):
         sel = nseg == k
         if sel.any():
