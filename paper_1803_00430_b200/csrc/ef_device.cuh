@@ -66,27 +66,38 @@ __device__ __forceinline__ void sample_sphere(uint32_t seed, uint32_t src, uint3
     }
 }
 
-// Direction of an accepted disk point (a, b), s = a^2 + b^2 < 1, lifted to
-// the cosine lobe about unit n with the Duff et al. ONB.
-__device__ __forceinline__ void cosine_dir(double a, double b, double s, double nx, double ny,
-                                           double nz, double& dx, double& dy, double& dz) {
-    const double z = sqrt(1.0 - s);
+// Duff et al. (2017) orthonormal basis (t1, t2) of unit n.  Computed once
+// per triangle (GpuShade); for the flipped normal -n the same expressions
+// give (t1, -t2) exactly (every product and quotient only changes sign).
+__device__ __forceinline__ void duff_onb(double nx, double ny, double nz, double* t1, double* t2) {
     const double sg = copysign(1.0, nz);
     const double aa = -1.0 / (sg + nz);
     const double bb = nx * ny * aa;
-    const double t1x = 1.0 + sg * nx * nx * aa, t1y = sg * bb, t1z = -sg * nx;
-    const double t2x = bb, t2y = sg + ny * ny * aa, t2z = -ny;
-    dx = (a * t1x + b * t2x) + z * nx;
-    dy = (a * t1y + b * t2y) + z * ny;
-    dz = (a * t1z + b * t2z) + z * nz;
+    t1[0] = 1.0 + sg * nx * nx * aa;
+    t1[1] = sg * bb;
+    t1[2] = -sg * nx;
+    t2[0] = bb;
+    t2[1] = sg + ny * ny * aa;
+    t2[2] = -ny;
 }
 
-// Cosine lobe about unit n: disk rejection (candidate j from draw 1 + j,
-// starting at candidate j0) + cosine_dir.
+// Direction of an accepted disk point (a, b), s = a^2 + b^2 < 1, lifted to
+// the cosine lobe about unit n with basis (t1, t2).
+__device__ __forceinline__ void cosine_dir(double a, double b, double s, double nx, double ny,
+                                           double nz, const double* t1, const double* t2,
+                                           double& dx, double& dy, double& dz) {
+    const double z = sqrt(1.0 - s);
+    dx = (a * t1[0] + b * t2[0]) + z * nx;
+    dy = (a * t1[1] + b * t2[1]) + z * ny;
+    dz = (a * t1[2] + b * t2[2]) + z * nz;
+}
+
+// Cosine lobe about unit n with basis (t1, t2): disk rejection (candidate j
+// from draw 1 + j, starting at candidate j0) + cosine_dir.
 __device__ __forceinline__ void sample_cosine(uint32_t seed, uint32_t src, uint32_t ray,
                                               uint32_t bounce, uint32_t frame, double nx, double ny,
-                                              double nz, double& dx, double& dy, double& dz,
-                                              uint32_t j0 = 0) {
+                                              double nz, const double* t1, const double* t2,
+                                              double& dx, double& dy, double& dz, uint32_t j0 = 0) {
     dx = nx; dy = ny; dz = nz;
     for (uint32_t j = j0; j < 64u; ++j) {
         double u1, u2;
@@ -95,7 +106,7 @@ __device__ __forceinline__ void sample_cosine(uint32_t seed, uint32_t src, uint3
         const double b = 2.0 * u2 - 1.0;
         const double s = a * a + b * b;
         if (s >= 1.0) continue;
-        cosine_dir(a, b, s, nx, ny, nz, dx, dy, dz);
+        cosine_dir(a, b, s, nx, ny, nz, t1, t2, dx, dy, dz);
         break;
     }
 }

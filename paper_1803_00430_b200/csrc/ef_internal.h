@@ -39,6 +39,17 @@ struct alignas(16) GpuTri {
 };
 static_assert(sizeof(GpuTri) == 80, "tri must be 80 bytes");
 
+// Per-triangle shading record by original id, 48 bytes: the normal, the
+// diffuse probability p_m of its material and the material index -- one
+// level of loads per reflection instead of material -> p_m.
+struct alignas(16) GpuShade {
+    double n[3];
+    double p;
+    int32_t m;
+    int32_t pad[3];
+};
+static_assert(sizeof(GpuShade) == 48, "shade record must be 48 bytes");
+
 struct HostBvh {
     std::vector<GpuNode> nodes;
     std::vector<int32_t> level_nodes;   // node indices grouped by depth (root level first)
@@ -64,6 +75,8 @@ namespace ef {
 // doubles apart; replaces the scene's nodes, leaf order and refit schedule.
 int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const double* e2,
                      int64_t stride, cudaStream_t st);
+// (Re)computes s->shade from s->normals, s->mat and s->pdiff (ef_scene.cu).
+int update_shade(ef_scene* s, cudaStream_t st);
 
 }  // namespace ef
 
@@ -86,6 +99,7 @@ struct ef_scene {
     float* fs = nullptr;               // (n_mat, n_bands) specular reflection factor
     double* pdiff = nullptr;           // (n_mat) probability of a diffuse bounce
     float* fr = nullptr;               // (n_mat, n_bands) (1 - a) * s for diffuse rain
+    ef::GpuShade* shade = nullptr;     // (n_tri) shading records, original order
     // refit support (dynamic scenes)
     int64_t* leaf_order = nullptr;     // (n_refs) leaf position -> original id
     int32_t* level_nodes = nullptr;    // node indices grouped by depth

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "ef_device.cuh"
 #include "ef_internal.h"
 
 using namespace ef;
@@ -35,12 +36,40 @@ void free_scene(ef_scene* s) {
     cudaFree(s->fs);
     cudaFree(s->pdiff);
     cudaFree(s->fr);
+    cudaFree(s->shade);
     cudaFree(s->leaf_order);
     cudaFree(s->level_nodes);
     delete s;
 }
 
+// Shading records (GpuShade) from the original-order normals and materials.
+__global__ void shade_kernel(GpuShade* out, const double* normals, const int32_t* mat,
+                             const double* pdiff, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        GpuShade r;
+        for (int k = 0; k < 3; ++k) r.n[k] = normals[3 * i + k];
+        r.m = mat[i];
+        r.p = pdiff[r.m];
+        r.pad[0] = r.pad[1] = r.pad[2] = 0;
+        out[i] = r;
+    }
+}
+
 }  // namespace
+
+int ef::update_shade(ef_scene* s, cudaStream_t st) {
+    if (s->n_tri == 0) return EF_OK;
+    if (!s->shade) {
+        cudaError_t e = cudaMalloc((void**)&s->shade, (size_t)s->n_tri * sizeof(GpuShade));
+        if (e != cudaSuccess) return check_cuda(e, "update_shade");
+        s->device_bytes += s->n_tri * (int64_t)sizeof(GpuShade);
+    }
+    shade_kernel<<<(int)std::min<int64_t>((s->n_tri + 255) / 256, 148 * 8), 256, 0, st>>>(
+        s->shade, s->normals, s->mat, s->pdiff, s->n_tri);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "shade_kernel");
+}
 
 extern "C" int ef_scene_create(const double* v0, const double* e1, const double* e2,
                                const double* normals, const int64_t* material_index, int64_t n_tri,
@@ -183,6 +212,12 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
             free_scene(s);
             return check_cuda(e, "ef_scene_create upload");
         }
+        const int rc = update_shade(s, nullptr);
+        if (rc == EF_OK) e = cudaStreamSynchronize(nullptr);
+        if (rc != EF_OK || e != cudaSuccess) {
+            free_scene(s);
+            return rc != EF_OK ? rc : check_cuda(e, "ef_scene_create shade");
+        }
     } catch (const std::exception& ex) {
         free_scene(s);
         return set_error(EF_EINVAL, std::string("ef_scene_create: ") + ex.what());
@@ -308,7 +343,8 @@ extern "C" int ef_scene_rebuild(ef_scene* s, const double* v0, const double* e1,
     copy_rows_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(
         s->tris_by_id, s->normals, v0, e1, e2, normals, n);
     count_launch();
-    const int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
+    int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
+    if (rc == EF_OK) rc = update_shade(s, st);
     if (rc != EF_OK) return rc;
     return device_build_bvh(s, v0, e1, e2, 3, st);
 }
@@ -323,6 +359,8 @@ extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, c
     update_tris_kernel<<<(int)std::min<int64_t>((nm + 255) / 256, 148 * 8), 256, 0, st>>>(
         s->tris, s->tris_by_id, s->normals, s->leaf_order, v0, e1, e2, normals, n, s->n_refs);
     count_launch();
+    const int rc = update_shade(s, st);
+    if (rc != EF_OK) return rc;
     const int levels = (int)s->level_start.size() - 1;
     for (int l = levels - 1; l >= 0; --l) {
         const int64_t a = s->level_start[l], cnt = s->level_start[l + 1] - a;
