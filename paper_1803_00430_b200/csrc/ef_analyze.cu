@@ -45,10 +45,13 @@ struct AnalyzeParams {
     int* counters;   // (n_sources) zeroed scratch, reset by the kernel
 };
 
-constexpr int kAThreads = 256;
+constexpr int kAThreads = 256;   // metrics_kernel
 constexpr int kAWarps = kAThreads / 32;
+constexpr int kKThreads = 512;   // analyze_kernel: 4 bins per thread at 2,000 bins
+constexpr size_t kMaxSeriesSmem = 96 * 1024;   // I_b(t) staged in shared memory up to 12,288 bins
 
 // block-wide sum of one double (all threads get the result)
+template <int T = kAThreads>
 __device__ __forceinline__ double block_sum(double v, double* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_sum(v);
@@ -57,8 +60,28 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     __syncthreads();
     double t = 0.0;
 #pragma unroll
-    for (int i = 0; i < kAWarps; ++i) t += red[i];
+    for (int i = 0; i < T / 32; ++i) t += red[i];
     return t;
+}
+
+// block-wide sums of N doubles with one pair of barriers (red: N * T/32)
+template <int N, int T>
+__device__ __forceinline__ void block_sum_n(double* v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < N; ++i) red[i * (T / 32) + w] = v[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < T / 32; ++k) t += red[i * (T / 32) + k];
+        v[i] = t;
+    }
 }
 
 struct Fit {
@@ -70,9 +93,11 @@ struct Fit {
 // (truncation) and LS line over EDC in [-35,-5] dB, or
 // [-25,-5] dB when the EDC does not reach -35 dB; every thread
 // owns the contiguous chunk [lo, hi) of I(t).  DESIGN.md 3.6.
-template <class F>
+// s_red holds >= 10 * T/32 doubles.
+template <int T, class F>
 __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_s, double* s_red,
                              double* s_dblast) {
+    constexpr int W = T / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
     Fit out{true, 0.0, 0.0};
@@ -90,7 +115,7 @@ __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_
     if (lane == 0) s_red[w] = suf;   // warp total
     __syncthreads();
     double after = 0.0, edc0 = 0.0;
-    for (int i = 0; i < kAWarps; ++i) {
+    for (int i = 0; i < W; ++i) {
         if (i > w) after += s_red[i];
         edc0 += s_red[i];
     }
@@ -113,10 +138,8 @@ __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_
             }
         }
     }
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int i = 0; i < 5; ++i) fit[r][i] = block_sum(fit[r][i], s_red);
+    __syncthreads();   // s_red is reused below
+    block_sum_n<10, T>(&fit[0][0], s_red);
     const double db_last = *s_dblast;
     const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
     if (r < 0) return out;
@@ -132,23 +155,26 @@ __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_
 }
 
 template <int ORDER>
-__global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams P) {
+__global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams P) {
     constexpr int NK = (ORDER + 1) * (ORDER + 1);
+    constexpr int T = kKThreads, W = T / 32;
+    extern __shared__ double s_I[];   // I_b(t), when n_bins fits (else read from H)
     __shared__ double s_B[kMaxDesign * NK];
     __shared__ double s_g[kMaxDesign];
     __shared__ double s_avg[NK];
-    __shared__ double s_red[kAWarps];
-    __shared__ double s_wsum[kAWarps][NK];
-    __shared__ int s_ired[3][kAWarps];
+    __shared__ double s_red[10 * W];
+    __shared__ double s_wsum[W][NK];
+    __shared__ int s_ired[3][W];
     __shared__ double s_dblast;
     __shared__ int s_done;
     const int nb = P.nb;
     const int s = blockIdx.x / nb, b = blockIdx.x % nb;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int nbins = P.n_bins;
+    const bool staged = (size_t)nbins * sizeof(double) <= kMaxSeriesSmem;
     const float* Hs = P.H + (size_t)s * nbins * nb * NK + (size_t)b * NK;
     const size_t stride = (size_t)nb * NK;
-    for (int j = tid; j < P.n_design; j += kAThreads) {
+    for (int j = tid; j < P.n_design; j += T) {
         double Y[NK];
         eval_sh<ORDER>(P.design[3 * j], P.design[3 * j + 1], P.design[3 * j + 2], Y);
 #pragma unroll
@@ -156,23 +182,38 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     }
     if (tid == 0) s_dblast = 0.0;
 
-    // ---- pass 1 (contiguous chunk per thread): support of I_b(t) =
-    // H[t,b,0]/Y00 and the directivity sums
-    const int chunk = (nbins + kAThreads - 1) / kAThreads;
+    // ---- pass 1 (contiguous chunk per thread, all its rows' loads in
+    // flight together): support of I_b(t) = H[t,b,0]/Y00, the directivity
+    // sums, and I_b(t) staged in shared memory for the fit
+    const int chunk = (nbins + T - 1) / T;
     const int lo = min(tid * chunk, nbins), hi = min(lo + chunk, nbins);
     int last = -1, first = INT_MAX, nnz = 0;
     double S[NK];
 #pragma unroll
     for (int k = 0; k < NK; ++k) S[k] = 0.0;
+#pragma unroll 4
     for (int t = lo; t < hi; ++t) {
         const float* row = Hs + t * stride;
-        if ((double)row[0] / kY00 > 0.0) {
+        float r[NK];
+        if constexpr (NK % 4 == 0) {   // rows are 16-byte aligned (stride and offset multiples of 4)
+#pragma unroll
+            for (int k = 0; k < NK; k += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(row + k));
+                r[k] = q.x; r[k + 1] = q.y; r[k + 2] = q.z; r[k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NK; ++k) r[k] = __ldg(row + k);
+        }
+        const double i0 = (double)r[0] / kY00;
+        if (staged) s_I[t] = i0;
+        if (i0 > 0.0) {
             last = t;
             first = min(first, t);
             ++nnz;
         }
 #pragma unroll
-        for (int k = 0; k < NK; ++k) S[k] += (double)row[k];
+        for (int k = 0; k < NK; ++k) S[k] += (double)r[k];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -192,7 +233,7 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     __syncthreads();
     last = -1; first = INT_MAX; nnz = 0;
 #pragma unroll
-    for (int i = 0; i < kAWarps; ++i) {
+    for (int i = 0; i < W; ++i) {
         last = max(last, s_ired[0][i]);
         first = min(first, s_ired[1][i]);
         nnz += s_ired[2][i];
@@ -200,15 +241,17 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     if (tid < NK) {
         double a = 0.0;
 #pragma unroll
-        for (int i = 0; i < kAWarps; ++i) a += s_wsum[i][tid];
+        for (int i = 0; i < W; ++i) a += s_wsum[i][tid];
         s_avg[tid] = a;   // raw sums for now
     }
     __syncthreads();
     const double total = s_avg[0] / kY00;
 
     // ---- pass 2: Schroeder fit (shared with the acoustic-metrics kernel)
-    const Fit fit = schroeder_fit([&](int t) { return (double)Hs[t * stride] / kY00; }, lo, hi, last,
-                                  nnz, P.bin_s, s_red, &s_dblast);
+    const Fit fit = staged
+        ? schroeder_fit<T>([&](int t) { return s_I[t]; }, lo, hi, last, nnz, P.bin_s, s_red, &s_dblast)
+        : schroeder_fit<T>([&](int t) { return (double)Hs[t * stride] / kY00; }, lo, hi, last, nnz,
+                           P.bin_s, s_red, &s_dblast);
     const bool silent = fit.silent;
     const double slope = fit.slope, nfit = fit.nfit;
     double rt60 = 1.0;   // cold-start value for silent bands
@@ -239,27 +282,36 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
     __syncthreads();
     if (tid < NK && P.avg_dir) P.avg_dir[((size_t)s * nb + b) * NK + tid] = s_avg[tid];
     if (P.loudness) {
-        for (int j = tid; j < P.n_design; j += kAThreads) {
+        for (int j = tid; j < P.n_design; j += T) {
             double g = 0.0;
 #pragma unroll
             for (int k = 0; k < NK; ++k) g += s_B[j * NK + k] * s_avg[k];
             s_g[j] = fmax(0.0, g);
         }
         __syncthreads();
+        // D = (4 pi / N) B^T diag(g) B: two adjacent lanes per entry, each
+        // summing half of the design, joined by one shuffle
         const double scale = 4.0 * M_PI / (double)P.n_design;
         double* D = P.loudness + ((size_t)s * nb + b) * NK * NK;
-        for (int e = tid; e < NK * NK; e += kAThreads) {
-            const int k1 = e / NK, k2 = e % NK;
+        const int half = (P.n_design + 1) / 2;
+        for (int base = 0; base < 2 * NK * NK; base += T) {   // block-uniform trip count
+            const int e2 = base + tid;
+            const bool ok = e2 < 2 * NK * NK;
+            const int e = e2 >> 1, k1 = e / NK, k2 = e % NK;
+            const int j0 = (e2 & 1) * half, j1 = ok ? min(P.n_design, j0 + half) : j0;
             double acc = 0.0;
-            for (int j = 0; j < P.n_design; ++j) acc += s_B[j * NK + k1] * s_g[j] * s_B[j * NK + k2];
-            D[e] = scale * acc;
+            for (int j = j0; j < j1; ++j) acc += s_B[j * NK + k1] * s_g[j] * s_B[j * NK + k2];
+            acc += __shfl_xor_sync(kAll, acc, 1);
+            if (ok && !(e2 & 1)) D[e] = scale * acc;
         }
     }
 
     // ---- per-source outputs: the last band block of a source finishes it
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_done = atomicAdd(P.counters + s, 1);
+    // (the finisher reads only the FIRST_BIN entries, written by thread 0)
+    if (tid == 0) {
+        __threadfence();
+        s_done = atomicAdd(P.counters + s, 1);
+    }
     __syncthreads();
     if (s_done == nb - 1 && tid == 0) {
         __threadfence();
@@ -282,7 +334,7 @@ __global__ void __launch_bounds__(kAThreads) analyze_kernel(const AnalyzeParams 
 __global__ void __launch_bounds__(kAThreads) metrics_kernel(const double* E, int n_bins, double bin_s,
                                                             const int32_t* direct_index, double e_ref,
                                                             double max_rt, double* out) {
-    __shared__ double s_red[kAWarps];
+    __shared__ double s_red[10 * kAWarps];
     __shared__ double s_dblast;
     __shared__ int s_ired[2][kAWarps];
     const int sr = blockIdx.x;
@@ -329,7 +381,8 @@ __global__ void __launch_bounds__(kAThreads) metrics_kernel(const double* E, int
     tsn = block_sum(tsn, s_red);
     if (tid == 0) s_dblast = 0.0;
     __syncthreads();
-    const Fit fit = schroeder_fit([&](int t) { return I[t]; }, lo, hi, last, nnz, bin_s, s_red, &s_dblast);
+    const Fit fit = schroeder_fit<kAThreads>([&](int t) { return I[t]; }, lo, hi, last, nnz, bin_s, s_red,
+                                             &s_dblast);
     if (tid == 0) {
         double* o = out + (size_t)sr * 5;
         o[0] = fit.silent ? -1.0 : fmin(fmax(-60.0 / fit.slope, 0.05), max_rt);
@@ -346,6 +399,12 @@ __global__ void blend_kernel(const float* cache, const float* frame,
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = a * frame[i] + b * cache[i];
+}
+
+template <int ORDER>
+static void analyze_set_smem() {
+    cudaFuncSetAttribute(analyze_kernel<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxSeriesSmem);
 }
 
 }  // namespace ef
@@ -396,13 +455,21 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
     if (e != cudaSuccess) return check_cuda(e, "ef_analyze scratch");
     AnalyzeParams P{H, Dir, stats, sum_t, design, loudness ? n_design : 0, cfg->n_bins, cfg->n_bands,
                     cfg->bin_s, cfg->max_rt, params, src_params, avg_dir, loudness, counters};
-    const dim3 grid(cfg->n_sources * cfg->n_bands), block(kAThreads);
+    const dim3 grid(cfg->n_sources * cfg->n_bands), block(kKThreads);
+    const size_t smem = (size_t)cfg->n_bins * sizeof(double) <= kMaxSeriesSmem
+                            ? (size_t)cfg->n_bins * sizeof(double) : 0;
+    static bool attr_done = false;
+    if (!attr_done) {   // the static shared tables plus up to 96 KB of series
+        analyze_set_smem<0>(); analyze_set_smem<1>(); analyze_set_smem<2>();
+        analyze_set_smem<3>(); analyze_set_smem<4>();
+        attr_done = true;
+    }
     switch (cfg->order) {
-        case 0: analyze_kernel<0><<<grid, block, 0, st>>>(P); break;
-        case 1: analyze_kernel<1><<<grid, block, 0, st>>>(P); break;
-        case 2: analyze_kernel<2><<<grid, block, 0, st>>>(P); break;
-        case 3: analyze_kernel<3><<<grid, block, 0, st>>>(P); break;
-        default: analyze_kernel<4><<<grid, block, 0, st>>>(P); break;
+        case 0: analyze_kernel<0><<<grid, block, smem, st>>>(P); break;
+        case 1: analyze_kernel<1><<<grid, block, smem, st>>>(P); break;
+        case 2: analyze_kernel<2><<<grid, block, smem, st>>>(P); break;
+        case 3: analyze_kernel<3><<<grid, block, smem, st>>>(P); break;
+        default: analyze_kernel<4><<<grid, block, smem, st>>>(P); break;
     }
     cudaError_t le = cudaGetLastError();
     cudaFreeAsync(counters, st);
