@@ -13,7 +13,7 @@ namespace ef {
 #ifdef EF_PROFILE_PHASES
 // debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
 // 2 pops after leaves, 3 shading, 4 segments)
-static __device__ unsigned long long g_phase[8];   // per translation unit
+static __device__ unsigned long long g_phase[12];   // per translation unit
 #define EF_PHASE_T0(v) const long long v = clock64()
 #define EF_PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(clock64() - (v)))
 #else

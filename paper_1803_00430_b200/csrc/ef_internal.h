@@ -15,6 +15,7 @@ constexpr int kBruteMaxTris = 512;   // scene.py:29
 constexpr double kRayEps = 1e-4;     // scene.py:22
 constexpr int kStackSize = 96;
 constexpr int kMaxLeaf = 4;
+constexpr int kTailMaxTris = 4096;   // scenes small enough for the CTA-wide tail sweep
 
 // Four-child BVH node, 128 bytes = eight 16-byte vectors, child boxes in
 // structure-of-arrays form so one node visit is 7 vector loads and four
@@ -75,7 +76,8 @@ namespace ef {
 // doubles apart; replaces the scene's nodes, leaf order and refit schedule.
 int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const double* e2,
                      int64_t stride, cudaStream_t st);
-// (Re)computes s->shade from s->normals, s->mat and s->pdiff (ef_scene.cu).
+// (Re)computes s->shade from s->normals, s->mat and s->pdiff, and s->tri_box
+// from s->tris_by_id and s->pad (ef_scene.cu).
 int update_shade(ef_scene* s, cudaStream_t st);
 
 }  // namespace ef
@@ -100,6 +102,8 @@ struct ef_scene {
     double* pdiff = nullptr;           // (n_mat) probability of a diffuse bounce
     float* fr = nullptr;               // (n_mat, n_bands) (1 - a) * s for diffuse rain
     ef::GpuShade* shade = nullptr;     // (n_tri) shading records, original order
+    float* tri_box = nullptr;          // (n_tri, 8) padded f32 triangle boxes lo.xyz hi.xyz,
+                                       // scenes of <= kTailMaxTris triangles (tail_kernel)
     // refit support (dynamic scenes)
     int64_t* leaf_order = nullptr;     // (n_refs) leaf position -> original id
     int32_t* level_nodes = nullptr;    // node indices grouped by depth

@@ -37,6 +37,7 @@ void free_scene(ef_scene* s) {
     cudaFree(s->pdiff);
     cudaFree(s->fr);
     cudaFree(s->shade);
+    cudaFree(s->tri_box);
     cudaFree(s->leaf_order);
     cudaFree(s->level_nodes);
     delete s;
@@ -56,6 +57,23 @@ __global__ void shade_kernel(GpuShade* out, const double* normals, const int32_t
     }
 }
 
+// Per-triangle f32 boxes over v0, v0+e1, v0+e2 rounded outward and padded
+// exactly like the BVH's leaf boxes, so the conservative slab test of a box
+// never drops a triangle the exact test would accept.
+__global__ void tribox_kernel(float* out, const double* tris, int64_t n, double pad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double* v = tris + 9 * i;
+        float* o = out + 8 * i;
+        for (int k = 0; k < 3; ++k) {
+            const double a = v[k], b = v[k] + v[3 + k], d = v[k] + v[6 + k];
+            o[k] = __double2float_rd(fmin(a, fmin(b, d)) - pad);
+            o[3 + k] = __double2float_ru(fmax(a, fmax(b, d)) + pad);
+        }
+        o[6] = o[7] = 0.0f;
+    }
+}
+
 }  // namespace
 
 int ef::update_shade(ef_scene* s, cudaStream_t st) {
@@ -68,6 +86,16 @@ int ef::update_shade(ef_scene* s, cudaStream_t st) {
     shade_kernel<<<(int)std::min<int64_t>((s->n_tri + 255) / 256, 148 * 8), 256, 0, st>>>(
         s->shade, s->normals, s->mat, s->pdiff, s->n_tri);
     count_launch();
+    if (s->n_tri <= kTailMaxTris) {
+        if (!s->tri_box) {
+            cudaError_t e = cudaMalloc((void**)&s->tri_box, (size_t)s->n_tri * 8 * sizeof(float));
+            if (e != cudaSuccess) return check_cuda(e, "update_shade");
+            s->device_bytes += s->n_tri * 8 * (int64_t)sizeof(float);
+        }
+        tribox_kernel<<<(int)((s->n_tri + 255) / 256), 256, 0, st>>>(s->tri_box, s->tris_by_id,
+                                                                      s->n_tri, s->pad);
+        count_launch();
+    }
     return check_cuda(cudaGetLastError(), "shade_kernel");
 }
 
@@ -344,9 +372,9 @@ extern "C" int ef_scene_rebuild(ef_scene* s, const double* v0, const double* e1,
         s->tris_by_id, s->normals, v0, e1, e2, normals, n);
     count_launch();
     int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
-    if (rc == EF_OK) rc = update_shade(s, st);
+    if (rc == EF_OK) rc = device_build_bvh(s, v0, e1, e2, 3, st);
     if (rc != EF_OK) return rc;
-    return device_build_bvh(s, v0, e1, e2, 3, st);
+    return update_shade(s, st);   // after the build: the boxes use its padding
 }
 
 extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, const double* e2,

@@ -118,6 +118,7 @@ struct TraceParams {
     const double* tris_by_id;
     int32_t n_tri;
     const GpuShade* shade;
+    const float* tri_box;
     const float* fd;
     const float* fs;
     int32_t nb;
@@ -150,6 +151,13 @@ struct TraceParams {
     int64_t er_cap;
     int32_t timing;         // debug: path_ids rows get (t0, t1, smid, nseg)
     int32_t smem_stack;     // traversal stack entries per thread kept in shared memory
+    // tail hand-off (tail_kernel): once the path counter is exhausted and at
+    // most tail_live paths are unfinished, they move to `cont` (0 = off)
+    int32_t tail_live;
+    unsigned long long* done;   // finished paths (warp-aggregated)
+    void* cont;                 // PathState<NBMAX>[tail_live]
+    unsigned int* cont_count;   // entries written to cont
+    unsigned int* cont_take;    // entries taken by tail_kernel
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -273,17 +281,22 @@ __device__ __forceinline__ LaneGroup lane_group() {
     return g;
 }
 
-// One segment of an active path: closest hit -> listener sphere and SH
-// histogram commit -> reflection.  With G > 1 the
-// group's lanes split the closest hit's triangle tests and the Philox draws;
-// everything else runs identically on each lane of the group.
+// The rest of a segment once its closest hit h is known: listener sphere and
+// SH histogram commit -> reflection.  With G > 1 the
+// group's lanes split the Philox draws (and diffuse-rain shadow rays on the
+// all-pairs path); everything else runs identically on each lane of the group.
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
+__device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
+                                               const Hit h, const double* s_tri, uint2* s_stack,
+                                               const LaneGroup& lg);
+
+// One segment of an active path: closest hit, then finish_segment.  With
+// G > 1 the group's lanes split the closest hit's triangle tests.
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
 __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                               const double* s_tri, uint2* s_stack,
                                               const LaneGroup& lg) {
-    const int nb = P.nb;
     const int gl = lg.gl;
-    const bool lead = lg.lead;
     // ---- closest hit (exact f64 leaf test)
     Hit h;
     if (BRUTE) {
@@ -299,6 +312,16 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
                                                   ls.c[EF_ST_TRIS], s_stack + threadIdx.x,
                                                   P.smem_stack);
     }
+    finish_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, h, s_tri, s_stack, lg);
+}
+
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
+__device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
+                                               const Hit h, const double* s_tri, uint2* s_stack,
+                                               const LaneGroup& lg) {
+    const int nb = P.nb;
+    const int gl = lg.gl;
+    const bool lead = lg.lead;
     const bool hit = h.id != INT32_MAX;
     EF_PHASE_T0(tsh);
     if (P.path_ids && !P.timing && lead) P.path_ids[S.path * P.max_bounces + S.nseg] = hit ? h.id : -1;
@@ -374,8 +397,8 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
                 } else {
                     sh = closest_bvh<(THREADS <= 512), SSTACK>(
                         P.nodes, P.tris, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit,
-                        ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], s_stack + threadIdx.x, P.smem_stack,
-                        true);
+                        ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], s_stack ? s_stack + threadIdx.x : nullptr,
+                        P.smem_stack, true);
                 }
                 if (sh.id == INT32_MAX && lead) {
                     const float gf = (float)(cosv * P.r2 / d2);
@@ -495,7 +518,28 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     S.last_diffuse = S.active = false;
     S.path = S.t_start = 0;
 
+    bool fin = false;                    // this lane's path ended in the last segment
+    unsigned long long done_seen = 0;    // P.done as read one iteration earlier
     for (;;) {
+        // ---- tail hand-off (P.tail_live > 0): count finished paths; once
+        // the path counter is exhausted and at most tail_live paths are
+        // unfinished, the warp's live paths move to the continuation list
+        // for tail_kernel, which runs each on a whole CTA
+        if (P.tail_live > 0) {
+            const unsigned fm = __ballot_sync(kFull, fin);
+            if (fm && lane == __ffs(fm) - 1) atomicAdd(P.done, (unsigned long long)__popc(fm));
+            fin = false;
+            if (__any_sync(kFull, exhausted)) {
+                if (S.active && P.total - done_seen <= (unsigned long long)P.tail_live) {
+                    const unsigned slot = atomicAdd(P.cont_count, 1u);
+                    if (slot < (unsigned)P.tail_live) {   // always: keep it otherwise
+                        reinterpret_cast<PathState<NBMAX>*>(P.cont)[slot] = S;
+                        S.active = false;
+                    }
+                }
+                done_seen = *reinterpret_cast<volatile unsigned long long*>(P.done);   // used next iteration
+            }
+        }
         // ---- warp-aggregated refill: idle lanes take the next path indices
         // (lane groups: only group leads count; a group's lanes share its
         // lead's path index)
@@ -542,6 +586,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         if (!live) break;
         if (!S.active) continue;
         trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, s_tri, s_stack, lg);
+        fin = !S.active;
     }
     if (lg.lead) flush_stats(ls, s_stats, s_sumt);
 
@@ -550,6 +595,151 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         if (s_stats[i]) atomicAdd(P.stats + i, (unsigned long long)s_stats[i]);
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x)
         if (s_sumt[i] != 0.0) atomicAdd(P.sum_t + i, s_sumt[i]);
+}
+
+// Tail of a frame (scenes of <= kTailMaxTris triangles): the paths handed off
+// by trace_kernel run one per CTA.  Every segment's closest hit is the
+// all-pairs answer (lowest id on equal t -- the same hit as the BVH's,
+// DESIGN.md 3.2) split over the CTA's 512 threads: an f32 slab test of each
+// triangle's padded box (conservative like the BVH's leaf boxes) picks the
+// candidates, the exact f64 test decides, and a (t, id) reduction joins the
+// threads; warp 0 then finishes the segment as a 32-lane group (parallel
+// draws).  A lone path's segment latency drops from a serial BVH walk (~3.1
+// us on C2) to one CTA-wide sweep.
+constexpr int kTailThreads = 512;
+
+// Triangle boxes staged in shared memory (32 B each, all of a <= 4,096-
+// triangle scene); the f64 triangles stay in L1 (staging them instead --
+// 72 B each -- shrinks L1 below the boxes' working set: 3.05 vs 2.44 us per
+// segment on C2).
+constexpr size_t kTailStageBytes = (size_t)kTailMaxTris * 32;
+
+template <int NBMAX, int ORDER>
+__global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams P) {
+    extern __shared__ __align__(16) float4 s_box[];   // (n_tri, 2) padded triangle boxes
+    __shared__ unsigned long long s_tb;   // closest t (bits of a positive double: ordered as u64)
+    __shared__ int s_id;                  // lowest id at that t
+    __shared__ int s_nc;                  // exact tests of the segment (counter EF_ST_TRIS)
+    __shared__ double s_ray[6];
+    __shared__ int s_active;
+    __shared__ unsigned s_j;
+    constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned n = min(*P.cont_count, (unsigned)P.tail_live);
+    if (blockIdx.x >= n) return;   // no path for this CTA
+    const PathState<NBMAX>* cont = reinterpret_cast<const PathState<NBMAX>*>(P.cont);
+    const LaneGroup lg = lane_group<32>();
+    {
+        const float4* src = reinterpret_cast<const float4*>(P.tri_box);
+#pragma unroll 4
+        for (int k = tid; k < 2 * P.n_tri; k += kTailThreads) s_box[k] = __ldg(src + k);
+    }
+    const double* tris = P.tris_by_id;
+    if (tid == 0) {
+        s_tb = kInfBits;
+        s_id = INT32_MAX;
+        s_nc = 0;
+    }
+    for (;;) {
+        if (tid == 0) s_j = atomicAdd(P.cont_take, 1u);
+        __syncthreads();
+        const unsigned j = s_j;
+        __syncthreads();
+        if (j >= n) break;
+        PathState<NBMAX> S = cont[j];   // warp 0 keeps the whole state, the others use o, d
+        LaneStats ls;
+        ls.src = S.src;
+        bool active = S.active;
+        double ox = S.ox, oy = S.oy, oz = S.oz, dx = S.dx, dy = S.dy, dz = S.dz;
+        while (active) {
+#ifdef EF_PROFILE_PHASES
+            const long long c0 = clock64();
+#endif
+            // ---- candidates by box, exact test, (t, id) minimum over the CTA
+            const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
+            const float tminf = fmaxf(__double2float_rd(kRayEps), 0.0f);
+            const float4* box = s_box;
+            Hit h{INFINITY, INT32_MAX};
+            int nc = 0;
+            for (int i0 = tid; i0 < P.n_tri; i0 += 4 * kTailThreads) {
+                uint32_t cand = 0;   // boxes of four triangles first, all loads in flight
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * kTailThreads;
+                    if (i < P.n_tri) {
+                        const float4 a = box[2 * i], b = box[2 * i + 1];
+                        if (slab_key_minmax(r, a.x, a.w, a.y, b.x, a.z, b.y, tminf, 1e38f, 0u) != 0xffffffffu)
+                            cand |= 1u << u;
+                    }
+                }
+                while (cand) {   // ascending ids: '<' keeps the lowest on equal t
+                    const int u = __ffs(cand) - 1;
+                    cand &= cand - 1u;
+                    const int i = i0 + u * kTailThreads;
+                    ++nc;
+                    double t;
+                    if (mt_hit(ox, oy, oz, dx, dy, dz, tris + 9 * i, kRayEps, INFINITY, t) && t < h.t) {
+                        h.t = t;
+                        h.id = i;
+                    }
+                }
+            }
+#ifdef EF_PROFILE_PHASES
+            const long long c1 = clock64();
+#endif
+            nc = __reduce_add_sync(kFull, nc);
+            if (h.id != INT32_MAX) atomicMin(&s_tb, (unsigned long long)__double_as_longlong(h.t));
+            if (lane == 0 && nc) atomicAdd(&s_nc, nc);
+            __syncthreads();
+            const unsigned long long tb = s_tb;
+            if (h.id != INT32_MAX && (unsigned long long)__double_as_longlong(h.t) == tb)
+                atomicMin(&s_id, h.id);
+            __syncthreads();
+#ifdef EF_PROFILE_PHASES
+            const long long c2 = clock64();
+#endif
+            if (w == 0) {
+                if (tb != kInfBits) {
+                    h.t = __longlong_as_double((long long)tb);
+                    h.id = s_id;
+                } else {
+                    h.t = INFINITY;
+                    h.id = INT32_MAX;
+                }
+                ls.c[EF_ST_TRIS] += (uint32_t)s_nc;
+                finish_segment<NBMAX, ORDER, false, kTailThreads, 32, false>(P, S, ls, h, nullptr, nullptr, lg);
+                if (lane == 0) {
+                    s_ray[0] = S.ox; s_ray[1] = S.oy; s_ray[2] = S.oz;
+                    s_ray[3] = S.dx; s_ray[4] = S.dy; s_ray[5] = S.dz;
+                    s_active = S.active;
+                    s_tb = kInfBits;
+                    s_id = INT32_MAX;
+                    s_nc = 0;
+                }
+            }
+#ifdef EF_PROFILE_PHASES
+            const long long c3 = clock64();
+#endif
+            __syncthreads();
+#ifdef EF_PROFILE_PHASES
+            if (tid == 0) {   // 8 sweep, 9 reduction, 10 finish_segment, 11 broadcast barrier
+                atomicAdd(&g_phase[8], (unsigned long long)(c1 - c0));
+                atomicAdd(&g_phase[9], (unsigned long long)(c2 - c1));
+                atomicAdd(&g_phase[10], (unsigned long long)(c3 - c2));
+                atomicAdd(&g_phase[11], (unsigned long long)(clock64() - c3));
+            }
+#endif
+            ox = s_ray[0]; oy = s_ray[1]; oz = s_ray[2];
+            dx = s_ray[3]; dy = s_ray[4]; dz = s_ray[5];
+            active = s_active != 0;
+        }
+        if (tid == 0 && ls.src >= 0) {
+#pragma unroll
+            for (int i = 0; i < EF_ST_COUNT; ++i)
+                if (ls.c[i]) atomicAdd(P.stats + ls.src * EF_ST_COUNT + i, (unsigned long long)ls.c[i]);
+            if (ls.sum_t != 0.0) atomicAdd(P.sum_t + ls.src, ls.sum_t);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -623,6 +813,33 @@ static int brute_group(unsigned long long paths, int n_tri) {
     int g = 16;
     while (g > 1 && ((unsigned long long)g * paths > cap || g / 2 >= n_tri)) g /= 2;
     return g == 2 ? 1 : g;   // no 2-lane instantiation
+}
+
+template <int NBMAX, int ORDER>
+static cudaError_t launch_tail_o(const TraceParams& P, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tail_kernel<NBMAX, ORDER>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const int grid = (int)std::max(1, std::min(P.tail_live, sm_count()));
+    const size_t smem = (size_t)P.n_tri * 32;   // n_tri <= kTailMaxTris (tail_live == 0 otherwise)
+    tail_kernel<NBMAX, ORDER><<<grid, kTailThreads, smem, st>>>(P);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int NBMAX>
+static cudaError_t launch_tail(int order, const TraceParams& P, cudaStream_t st) {
+    switch (order) {
+        case 0: return launch_tail_o<NBMAX, 0>(P, st);
+        case 1: return launch_tail_o<NBMAX, 1>(P, st);
+        case 2: return launch_tail_o<NBMAX, 2>(P, st);
+        case 3: return launch_tail_o<NBMAX, 3>(P, st);
+        default: return launch_tail_o<NBMAX, 4>(P, st);
+    }
 }
 
 template <int NBMAX>
@@ -866,13 +1083,25 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
         if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
     }
-    unsigned long long* counter = nullptr;
+    // tail hand-off for small BVH scenes (tail_kernel): at most one CTA per
+    // SM of paths; EF_TAIL_LIVE overrides the threshold (0 = off; tuning)
+    static const int tail_env = [] {
+        const char* v = std::getenv("EF_TAIL_LIVE");
+        return v ? std::atoi(v) : -1;
+    }();
+    const int tail_live = (brute || s->n_tri > kTailMaxTris || !s->tri_box) ? 0
+                          : (tail_env >= 0 ? tail_env : sm_count());
+    // scratch: path counter, finished paths, continuation count / take, then
+    // the continuation list
+    constexpr size_t kHdr = 32;
+    unsigned char* scratch = nullptr;
     keep_pool_memory();
-    e = cudaMallocAsync((void**)&counter, sizeof(unsigned long long), st);
+    e = cudaMallocAsync((void**)&scratch, kHdr + (size_t)tail_live * sizeof(PathState<8>), st);
     if (e != cudaSuccess) return check_cuda(e, "cudaMallocAsync");
+    unsigned long long* counter = reinterpret_cast<unsigned long long*>(scratch);
     for (int s0 = 0; s0 < cfg->n_sources; s0 += kMaxSourcesPerLaunch) {
         const int ns = std::min(kMaxSourcesPerLaunch, cfg->n_sources - s0);
-        e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+        e = cudaMemsetAsync(scratch, 0, kHdr, st);
         if (e != cudaSuccess) break;
         TraceParams P;
         P.nodes = s->nodes;
@@ -880,6 +1109,7 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.tris_by_id = s->tris_by_id;
         P.n_tri = (int32_t)s->n_tri;
         P.shade = s->shade;
+        P.tri_box = s->tri_box;
         P.fd = s->fd;
         P.fs = s->fs;
         P.nb = s->n_bands;
@@ -926,6 +1156,11 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.er_cap = cfg->er_capacity;
         P.counter = counter;
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
+        P.tail_live = tail_live;
+        P.done = counter + 1;
+        P.cont_count = reinterpret_cast<unsigned int*>(scratch + 16);
+        P.cont_take = reinterpret_cast<unsigned int*>(scratch + 20);
+        P.cont = scratch + kHdr;
         static const int force_big = [] {
             const char* e = std::getenv("EF_TRACE_BIG");   // tuning only: 0 / 1
             return e ? std::atoi(e) : -1;
@@ -944,13 +1179,16 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
                                     (size_t)ns * (EF_ST_COUNT * 4 + 8) + 64;
         P.smem_stack = (!brute && !big && sstack_env && max_stack <= kStackSize &&
                         sstack_bytes <= kMaxSstackBytes) ? max_stack : 0;
-        if (s->n_bands <= 4)
+        if (s->n_bands <= 4) {
             e = dispatch<4>(brute, big, cfg->order, P, st);
-        else
+            if (e == cudaSuccess && tail_live > 0) e = launch_tail<4>(cfg->order, P, st);
+        } else {
             e = dispatch<8>(brute, big, cfg->order, P, st);
+            if (e == cudaSuccess && tail_live > 0) e = launch_tail<8>(cfg->order, P, st);
+        }
         if (e != cudaSuccess) break;
     }
-    cudaError_t e2 = cudaFreeAsync(counter, st);
+    cudaError_t e2 = cudaFreeAsync(scratch, st);
     if (e != cudaSuccess) return check_cuda(e, "trace_kernel");
     return check_cuda(e2, "cudaFreeAsync");
 }
@@ -1013,9 +1251,9 @@ extern "C" int ef_loudness_batch(const double* avg, int64_t n, int32_t order, co
 
 #ifdef EF_PROFILE_PHASES
 extern "C" int ef_debug_phases(unsigned long long* out8, int reset) {
-    cudaMemcpyFromSymbol(out8, g_phase, sizeof(unsigned long long) * 8);
+    cudaMemcpyFromSymbol(out8, g_phase, sizeof(unsigned long long) * 12);
     if (reset) {
-        unsigned long long z[8] = {0};
+        unsigned long long z[12] = {0};
         cudaMemcpyToSymbol(g_phase, z, sizeof z);
     }
     return EF_OK;

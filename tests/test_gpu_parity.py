@@ -272,6 +272,24 @@ def test_c2_city_subsample_parity():
     assert total_excl <= 8 * n * 0.01
 
 
+def test_c2_tail_kernel_paths_exact():
+    """The frame's last paths run in tail_kernel (CTA-wide candidate sweep):
+    C2's 100-bounce path (source 6, ray 27707) alone -- handed off at once,
+    so no BVH node is visited -- and with 299 neighbours, ids and bounce
+    counts equal to the oracle's."""
+    w = workloads.c2_city()
+    os_ = _oracle_for(w)
+    for rays in (np.array([27707], np.uint32), np.arange(27600, 27900, dtype=np.uint32)):
+        _, _, tr = _run_gpu(w, ray_ids=rays, sources=[6])
+        ref = _oracle_trace(os_, w, 6, rays)
+        bad, excl = _compare_paths(tr.path_nseg.cpu().numpy()[0], tr.path_ids.cpu().numpy()[0], ref)
+        assert bad == 0 and excl <= 3
+        if len(rays) == 1:
+            st = tr.stats.cpu().numpy()[0]
+            assert tr.path_nseg.cpu().numpy()[0, 0] == 100 == st[1]
+            assert st[7] < st[1]   # ~no node visits: every segment came from the tail sweep
+
+
 def test_c2_matches_reference_driven_golden(golden):
     g = golden("c2_city")
     w = workloads.c2_city()

@@ -162,7 +162,7 @@ def phases(name="c2", src=6, ray=27707):
                                   bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
     tr = propagation.FrameTracer(sc, 1, cfg, record=2)
     tr.set_sources(w.sources[src:src + 1], [src])
-    out = np.zeros(8, np.uint64)
+    out = np.zeros(12, np.uint64)
     for rep in range(3):
         L.ef_debug_phases(out.ctypes.data, 1)
         tr.trace(w.listener, ray_ids=[ray])
@@ -172,6 +172,8 @@ def phases(name="c2", src=6, ray=27707):
     names = ["inner visits", "leaf tests", "pops after leaf", "shading"]
     print(f"[{name}] path src {src} ray {ray}: {segs} segments; cycles per segment:")
     for i, n in enumerate(names):
+        print(f"   {n:16s} {int(out[i]) / max(segs, 1):9.0f}")
+    for i, n in zip(range(8, 12), ["tail sweep", "tail reduction", "tail finish", "tail barrier"]):
         print(f"   {n:16s} {int(out[i]) / max(segs, 1):9.0f}")
 
 
