@@ -45,6 +45,7 @@ constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr size_t kMaxSstackBytes = 128 * 1024;   // leave >= 128 KB of the SM's 256 KB to L1
 constexpr int kMaxSourcesPerLaunch = 256;
 constexpr int kMaxRanks = 8;   // GPUs of one node reachable by ef_trace_fused
+constexpr int kTailLongSegs = 16;   // tail hand-off: paths with this many segments are taken first
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
@@ -156,8 +157,8 @@ struct TraceParams {
     int32_t tail_live;
     unsigned long long* done;   // finished paths (warp-aggregated)
     void* cont;                 // PathState<NBMAX>[tail_live]
-    unsigned int* cont_count;   // entries written to cont
-    unsigned int* cont_take;    // entries taken by tail_kernel
+    unsigned int* cont_count;   // [0] long paths (cont[0..)), [1] short ones (cont[tail_live-1..] down)
+    unsigned int* cont_take;    // entries taken by tail_kernel (long ones first)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -531,8 +532,12 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
             fin = false;
             if (__any_sync(kFull, exhausted)) {
                 if (S.active && P.total - done_seen <= (unsigned long long)P.tail_live) {
-                    const unsigned slot = atomicAdd(P.cont_count, 1u);
-                    if (slot < (unsigned)P.tail_live) {   // always: keep it otherwise
+                    // paths already long go first (the frame's critical chain
+                    // starts at once), the rest fill the list from its end
+                    const bool lng = S.nseg >= kTailLongSegs;
+                    const unsigned k = atomicAdd(P.cont_count + (lng ? 0 : 1), 1u);
+                    const unsigned slot = lng ? k : (unsigned)P.tail_live - 1u - k;
+                    if (k < (unsigned)P.tail_live) {   // always: at most tail_live paths are unfinished
                         reinterpret_cast<PathState<NBMAX>*>(P.cont)[slot] = S;
                         S.active = false;
                     }
@@ -625,7 +630,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
     __shared__ unsigned s_j;
     constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const unsigned n = min(*P.cont_count, (unsigned)P.tail_live);
+    const unsigned n_long = min(P.cont_count[0], (unsigned)P.tail_live);
+    const unsigned n = min(n_long + P.cont_count[1], (unsigned)P.tail_live);
     if (blockIdx.x >= n) return;   // no path for this CTA
     const PathState<NBMAX>* cont = reinterpret_cast<const PathState<NBMAX>*>(P.cont);
     const LaneGroup lg = lane_group<32>();
@@ -646,7 +652,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
         const unsigned j = s_j;
         __syncthreads();
         if (j >= n) break;
-        PathState<NBMAX> S = cont[j];   // warp 0 keeps the whole state, the others use o, d
+        // long paths first (front of the list), then the short ones (back)
+        PathState<NBMAX> S = cont[j < n_long ? j : (unsigned)P.tail_live - 1u - (j - n_long)];
         LaneStats ls;
         ls.src = S.src;
         bool active = S.active;
@@ -1083,16 +1090,18 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
         if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
     }
-    // tail hand-off for small BVH scenes (tail_kernel): at most one CTA per
-    // SM of paths; EF_TAIL_LIVE overrides the threshold (0 = off; tuning)
+    // tail hand-off for small BVH scenes (tail_kernel): at most two paths
+    // per SM (C2 sweep 32..592: 296 best, 1.53 vs 1.40 G seg/s without;
+    // larger lists make whole CTAs run short paths one segment at a time);
+    // EF_TAIL_LIVE overrides the threshold (0 = off; tuning)
     static const int tail_env = [] {
         const char* v = std::getenv("EF_TAIL_LIVE");
         return v ? std::atoi(v) : -1;
     }();
     const int tail_live = (brute || s->n_tri > kTailMaxTris || !s->tri_box) ? 0
-                          : (tail_env >= 0 ? tail_env : sm_count());
-    // scratch: path counter, finished paths, continuation count / take, then
-    // the continuation list
+                          : (tail_env >= 0 ? tail_env : 2 * sm_count());
+    // scratch header: path counter (u64), finished paths (u64), continuation
+    // counts (u32 long, u32 short), entries taken (u32); then the list
     constexpr size_t kHdr = 32;
     unsigned char* scratch = nullptr;
     keep_pool_memory();
@@ -1158,8 +1167,8 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.total = (unsigned long long)ns * (unsigned long long)cfg->n_rays;
         P.tail_live = tail_live;
         P.done = counter + 1;
-        P.cont_count = reinterpret_cast<unsigned int*>(scratch + 16);
-        P.cont_take = reinterpret_cast<unsigned int*>(scratch + 20);
+        P.cont_count = reinterpret_cast<unsigned int*>(scratch + 16);   // [0], [1]
+        P.cont_take = reinterpret_cast<unsigned int*>(scratch + 24);
         P.cont = scratch + kHdr;
         static const int force_big = [] {
             const char* e = std::getenv("EF_TRACE_BIG");   // tuning only: 0 / 1

@@ -77,10 +77,11 @@ def main():
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd *= scale.get(m["dram__bytes_read.sum"][1], 1)
     wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
-    os.makedirs("profiles", exist_ok=True)
-    json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": rep,
+    outdir = os.environ.get("EF_TRAFFIC_DIR", "profiles")   # on the GPU box: a gpurun_out/ subdir
+    os.makedirs(outdir, exist_ok=True)
+    json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": os.path.basename(rep),
                "note": f"one ncu --set full capture of {name.split('(')[0]}"},
-              open(os.path.join("profiles", f"traffic_{config}.json"), "w"), indent=1)
+              open(os.path.join(outdir, f"traffic_{config}.json"), "w"), indent=1)
     print("\n".join(lines))
     print("\n".join(body))
 
