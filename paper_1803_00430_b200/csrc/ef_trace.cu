@@ -349,6 +349,10 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         S.active = false;
     } else {
         // ---- reflection
+#ifdef EF_PROFILE_PHASES
+        const long long fa = clock64();   // tail profile (G == 32): listener part
+        if (G == 32 && lead) atomicAdd(&g_phase[0], (unsigned long long)(fa - tsh));
+#endif
         const double t = h.t;
         S.plen += t;
         ls.sum_t += t;
@@ -376,6 +380,10 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         }
         const bool diffuse = u1 < pdiff;
         const double nd = dot3(nx, ny, nz, S.dx, S.dy, S.dz);
+#ifdef EF_PROFILE_PHASES
+        const long long fb = clock64();   // shading record + draws
+        if (G == 32 && lead) atomicAdd(&g_phase[1], (unsigned long long)(fb - fa));
+#endif
         if (P.rain && diffuse) {
             // ---- diffuse rain: connect this bounce to the listener
             // centre; Lambertian lobe through the receiver cross-section:
@@ -451,6 +459,9 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
             S.dz = S.dz - k2 * nz;
         }
         if (S.nrefl >= P.max_bounces) S.active = false;
+#ifdef EF_PROFILE_PHASES
+        if (G == 32 && lead) atomicAdd(&g_phase[2], (unsigned long long)(clock64() - fb));   // direction
+#endif
     }
     EF_PHASE_ADD(3, tsh);
 #ifdef EF_PROFILE_PHASES

@@ -151,7 +151,10 @@ if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "knobs":
 
 
 def phases(name="c2", src=6, ray=27707):
-    """Cycle breakdown of one path (needs EF_LIB_PATH=..._prof.so)."""
+    """Cycle breakdown of one path (needs EF_LIB_PATH=..._prof.so).  Segments
+    run by tail_kernel report the tail phases; their finish_segment splits
+    into counters 0-2 (listener / shading record + draws / direction), which
+    the BVH path uses for visits / leaf tests / pops."""
     import ctypes
     from paper_1803_00430_b200 import _lib
     L = _lib.lib()
