@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 
 #include "ef_device.cuh"
 
@@ -66,7 +68,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // block-wide sums of N doubles with one pair of barriers (red: N * T/32)
 template <int N, int T>
-__device__ __forceinline__ void block_sum_n(double* v, double* red) {
+__device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
@@ -99,7 +101,9 @@ __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_
                              double* s_dblast) {
     constexpr int W = T / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double fit[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};  // n, sx, sy, sxy, sxx
+    // n, sx, sy, sxy, sxx for the [-35,-5] (0..4) and [-25,-5] (5..9) ranges;
+    // a flat array indexed by constants only, so it stays in registers
+    double fit[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     Fit out{true, 0.0, 0.0};
     if (nnz < 3) return out;
     const int h2 = min(hi, last + 1);
@@ -130,20 +134,21 @@ __device__ Fit schroeder_fit(F I, int lo, int hi, int last, int nnz, double bin_
         for (int r = 0; r < 2; ++r) {
             const double lim = r == 0 ? -35.0 : -25.0;
             if (db <= -5.0 && db >= lim) {
-                fit[r][0] += 1.0;
-                fit[r][1] += x;
-                fit[r][2] += db;
-                fit[r][3] += x * db;
-                fit[r][4] += x * x;
+                fit[5 * r + 0] += 1.0;
+                fit[5 * r + 1] += x;
+                fit[5 * r + 2] += db;
+                fit[5 * r + 3] += x * db;
+                fit[5 * r + 4] += x * x;
             }
         }
     }
     __syncthreads();   // s_red is reused below
-    block_sum_n<10, T>(&fit[0][0], s_red);
+    block_sum_n<10, T>(fit, s_red);
     const double db_last = *s_dblast;
     const int r = db_last <= -35.0 ? 0 : (db_last <= -25.0 ? 1 : -1);
     if (r < 0) return out;
-    const double n = fit[r][0], sx = fit[r][1], sy = fit[r][2], sxy = fit[r][3], sxx = fit[r][4];
+    const double n = r ? fit[5] : fit[0], sx = r ? fit[6] : fit[1], sy = r ? fit[7] : fit[2],
+                 sxy = r ? fit[8] : fit[3], sxx = r ? fit[9] : fit[4];
     const double den = n * sxx - sx * sx;
     if (n < 2.0 || !(den > 0.0)) return out;
     const double slope = (n * sxy - sx * sy) / den;
@@ -401,6 +406,31 @@ __global__ void blend_kernel(const float* cache, const float* frame,
         out[i] = a * frame[i] + b * cache[i];
 }
 
+// Per-stream "source finished" counters for analyze_kernel: zeroed once when
+// allocated and left zeroed by the kernel itself (its last CTA per source
+// resets its entry), so a call needs no allocation or memset.  Calls on one
+// stream are ordered; different streams get different buffers.
+static int* analyze_counters(cudaStream_t st, int n, cudaError_t& e) {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, std::pair<int*, int>> bufs;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& b = bufs[st];
+    if (b.second < n) {
+        if (b.first) {
+            e = cudaFreeAsync(b.first, st);
+            if (e != cudaSuccess) return nullptr;
+        }
+        b = {nullptr, 0};
+        const int cap = std::max(n, 256);
+        e = cudaMallocAsync((void**)&b.first, sizeof(int) * cap, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(b.first, 0, sizeof(int) * cap, st);
+        if (e != cudaSuccess) return nullptr;
+        b.second = cap;
+    }
+    e = cudaSuccess;
+    return b.first;
+}
+
 template <int ORDER>
 static void analyze_set_smem() {
     cudaFuncSetAttribute(analyze_kernel<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -448,11 +478,10 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
         return set_error(EF_EINVAL, "ef_analyze: loudness needs a t-design of 1..64 directions");
     if (!(cfg->bin_s > 0.0) || !(cfg->max_rt >= 0.05)) return set_error(EF_EINVAL, "ef_analyze: bad bin_s / max_rt");
     cudaStream_t st = (cudaStream_t)stream;
-    int* counters = nullptr;
     keep_pool_memory();
-    cudaError_t e = cudaMallocAsync((void**)&counters, sizeof(int) * cfg->n_sources, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, sizeof(int) * cfg->n_sources, st);
-    if (e != cudaSuccess) return check_cuda(e, "ef_analyze scratch");
+    cudaError_t e = cudaSuccess;
+    int* counters = analyze_counters(st, cfg->n_sources, e);
+    if (!counters) return check_cuda(e, "ef_analyze scratch");
     AnalyzeParams P{H, Dir, stats, sum_t, design, loudness ? n_design : 0, cfg->n_bins, cfg->n_bands,
                     cfg->bin_s, cfg->max_rt, params, src_params, avg_dir, loudness, counters};
     const dim3 grid(cfg->n_sources * cfg->n_bands), block(kKThreads);
@@ -472,7 +501,6 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
         default: analyze_kernel<4><<<grid, block, smem, st>>>(P); break;
     }
     cudaError_t le = cudaGetLastError();
-    cudaFreeAsync(counters, st);
     count_launch();
     return check_cuda(le, "analyze_kernel");
 }
