@@ -780,7 +780,11 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     // chain shares its SM with as few others as possible.
     const long long sms = (long long)sm_count();
     const long long lanes = (long long)P.total * G;
-    int block = THREADS;
+    static const int block_env = [] {   // tuning only: threads per CTA (<= THREADS)
+        const char* e = std::getenv("EF_BLOCK");
+        return e ? std::atoi(e) : 0;
+    }();
+    int block = (block_env >= 32 && block_env <= THREADS) ? block_env / 32 * 32 : THREADS;
     if (lanes < sms * THREADS) {
         const long long per = (lanes + sms - 1) / sms;
         block = (int)std::min<long long>(THREADS, std::max<long long>(32, (per + 31) / 32 * 32));
