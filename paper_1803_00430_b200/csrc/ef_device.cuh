@@ -305,7 +305,9 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
                                           double t_min, Hit& h, float& tb, uint32_t& n_tris) {
     const uint32_t e = ~(uint32_t)enc;
     const uint32_t start = e >> 3, cnt = (e & 7u) + 1u;
+#ifndef EF_NO_WORK_COUNTERS
     n_tris += cnt;
+#endif
     for (uint32_t i = 0; i < cnt; ++i) {
         const double2* q = reinterpret_cast<const double2*>(tris + start + i);
         const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3),
@@ -453,7 +455,9 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     for (;;) {
         while (node >= 0) {
             EF_PHASE_T0(tv);
+#ifndef EF_NO_WORK_COUNTERS
             ++n_nodes;
+#endif
             const float4* q = reinterpret_cast<const float4*>(nodes + node);
             uint32_t k0, k1, k2, k3;
             int4 ch;

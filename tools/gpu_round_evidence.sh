@@ -17,6 +17,11 @@ for c in c1 c3 c5; do
   timeout 1500 python bench.py --config $c --steps $st --warmup 3 > $O/${TAG}_bench_$c.jsonl 2> $O/${TAG}_bench_$c.err
 done
 timeout 1500 python bench.py --config c4 --steps 20 --warmup 3 > $O/${TAG}_bench_c4.jsonl 2> $O/${TAG}_bench_c4.err
+# step anatomy and C2's longest path (timing build of the trace: per-path clocks)
+for c in c1 c2; do python tools/probe_step.py $c >> $O/${TAG}_step_anatomy.txt 2>&1; done
+python tools/probe_trace.py c2 timing > $O/${TAG}_c2_path_timing.txt 2>&1
+python tools/probe_trace.py c2 single >> $O/${TAG}_c2_path_timing.txt 2>&1
+EF_TAIL_LIVE=0 python tools/probe_trace.py c2 single >> $O/${TAG}_c2_path_timing.txt 2>&1
 # launch lists + one full capture per hot kernel, summarised here
 for c in c1 c2; do
   B="python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline"
