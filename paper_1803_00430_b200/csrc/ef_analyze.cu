@@ -23,6 +23,9 @@
 namespace ef {
 
 constexpr unsigned kAll = 0xffffffffu;
+#ifdef EF_PROFILE_PHASES
+static __device__ long long g_t0;   // kernel start (block 0, thread 0)
+#endif
 constexpr double kY00 = 0.28209479177387814;   // sh.py:17
 constexpr int kMaxDesign = 64;    // design_for_order(<=4) has 48 points
 
@@ -172,6 +175,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
     __shared__ int s_ired[3][W];
     __shared__ double s_dblast;
     __shared__ int s_done;
+#ifdef EF_PROFILE_PHASES
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_t0 = clock64();
+#endif
     const int nb = P.nb;
     const int s = blockIdx.x / nb, b = blockIdx.x % nb;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -187,6 +193,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
     }
     if (tid == 0) s_dblast = 0.0;
 
+#ifdef EF_PROFILE_PHASES
+    const long long a0 = clock64();   // analysis phases (counters of the analysis TU)
+#endif
     // ---- pass 1 (contiguous chunk per thread, all its rows' loads in
     // flight together): support of I_b(t) = H[t,b,0]/Y00, the directivity
     // sums, and I_b(t) staged in shared memory for the fit
@@ -220,6 +229,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
 #pragma unroll
         for (int k = 0; k < NK; ++k) S[k] += (double)r[k];
     }
+#ifdef EF_PROFILE_PHASES
+    if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_phase[5], (unsigned long long)(clock64() - a0));
+#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         last = max(last, __shfl_xor_sync(kAll, last, o));
@@ -228,6 +240,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
     }
 #pragma unroll
     for (int k = 0; k < NK; ++k) S[k] = warp_sum(S[k]);
+#ifdef EF_PROFILE_PHASES
+    if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_phase[6], (unsigned long long)(clock64() - a0));
+#endif
     if (lane == 0) {
         s_ired[0][w] = last;
         s_ired[1][w] = first;
@@ -252,6 +267,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
     __syncthreads();
     const double total = s_avg[0] / kY00;
 
+#ifdef EF_PROFILE_PHASES
+    const long long a1 = clock64();
+#endif
     // ---- pass 2: Schroeder fit (shared with the acoustic-metrics kernel)
     const Fit fit = staged
         ? schroeder_fit<T>([&](int t) { return s_I[t]; }, lo, hi, last, nnz, P.bin_s, s_red, &s_dblast)
@@ -281,6 +299,9 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
         p[EF_P_LAST_BIN] = (double)last;
     }
 
+#ifdef EF_PROFILE_PHASES
+    const long long a2 = clock64();
+#endif
     // ---- average directivity and loudness (sh.py:240-253)
     __syncthreads();
     if (tid < NK) s_avg[tid] = total > 0.0 ? s_avg[tid] / total : 0.0;
@@ -311,6 +332,16 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
         }
     }
 
+#ifdef EF_PROFILE_PHASES
+    if (tid == 0 && blockIdx.x == 0) {
+        const long long a3 = clock64();
+        atomicAdd(&g_phase[0], (unsigned long long)(a1 - a0));
+        atomicAdd(&g_phase[1], (unsigned long long)(a2 - a1));
+        atomicAdd(&g_phase[2], (unsigned long long)(a3 - a2));
+        atomicAdd(&g_phase[3], 1ull);
+        atomicAdd(&g_phase[4], (unsigned long long)(a0 - g_t0));
+    }
+#endif
     // ---- per-source outputs: the last band block of a source finishes it
     // (the finisher reads only the FIRST_BIN entries, written by thread 0)
     if (tid == 0) {
@@ -430,6 +461,21 @@ static int* analyze_counters(cudaStream_t st, int n, cudaError_t& e) {
     e = cudaSuccess;
     return b.first;
 }
+
+#ifdef EF_PROFILE_PHASES
+}  // namespace ef
+// debug builds: [0] pass 1, [1] fit, [2] directivity + loudness, [3] calls,
+// [4] start -> pass 1, [5] pass-1 rows done, [6] pass-1 warp sums done
+extern "C" int ef_debug_analysis_phases(unsigned long long* out7, int reset) {
+    cudaMemcpyFromSymbol(out7, ef::g_phase, sizeof(unsigned long long) * 7);
+    if (reset) {
+        unsigned long long z[12] = {0};
+        cudaMemcpyToSymbol(ef::g_phase, z, sizeof z);
+    }
+    return EF_OK;
+}
+namespace ef {
+#endif
 
 template <int ORDER>
 static void analyze_set_smem() {
