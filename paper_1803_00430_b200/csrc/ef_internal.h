@@ -16,6 +16,7 @@ constexpr double kRayEps = 1e-4;     // scene.py:22
 constexpr int kStackSize = 96;
 constexpr int kMaxLeaf = 4;
 constexpr int kTailMaxTris = 4096;   // scenes small enough for the CTA-wide tail sweep
+constexpr int kTailCluster = 16;     // leaf-order triangles per tail-sweep cluster
 
 // Four-child BVH node, 128 bytes = eight 16-byte vectors, child boxes in
 // structure-of-arrays form so one node visit is 7 vector loads and four
@@ -104,6 +105,11 @@ struct ef_scene {
     ef::GpuShade* shade = nullptr;     // (n_tri) shading records, original order
     float* tri_box = nullptr;          // (n_tri, 8) padded f32 triangle boxes lo.xyz hi.xyz,
                                        // scenes of <= kTailMaxTris triangles (tail_kernel)
+    float* clu_box = nullptr;          // (n_clu, 8) unions of kTailCluster consecutive leaf-order boxes
+    int32_t* clu_ids = nullptr;        // (n_tri) triangle ids in leaf order, each once
+    int64_t n_clu = 0;
+    std::vector<int32_t> clu_order;    // host builds: that order (spatial splits repeat ids
+                                       // in the leaves); empty: the device tree's leaf order
     // refit support (dynamic scenes)
     int64_t* leaf_order = nullptr;     // (n_refs) leaf position -> original id
     int32_t* level_nodes = nullptr;    // node indices grouped by depth

@@ -38,6 +38,8 @@ void free_scene(ef_scene* s) {
     cudaFree(s->fr);
     cudaFree(s->shade);
     cudaFree(s->tri_box);
+    cudaFree(s->clu_box);
+    cudaFree(s->clu_ids);
     cudaFree(s->leaf_order);
     cudaFree(s->level_nodes);
     delete s;
@@ -74,6 +76,35 @@ __global__ void tribox_kernel(float* out, const double* tris, int64_t n, double 
     }
 }
 
+// Clusters of kTailCluster consecutive leaf-order triangles (spatially
+// coherent runs): the union of their padded boxes (still conservative) and
+// their ids, for the tail sweep's first level.
+__global__ void order_kernel(int32_t* clu_ids, const int64_t* leaf_order, int64_t n) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        clu_ids[r] = (int32_t)leaf_order[r];
+}
+
+__global__ void cluster_kernel(float* clu_box, const int32_t* clu_ids, const float* tri_box,
+                               int64_t n_ids, int64_t n_clu) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_clu;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t r = c * kTailCluster; r < n_ids && r < (c + 1) * kTailCluster; ++r) {
+            const int64_t id = clu_ids[r];
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = fminf(lo[k], tri_box[8 * id + k]);
+                hi[k] = fmaxf(hi[k], tri_box[8 * id + 3 + k]);
+            }
+        }
+        float* o = clu_box + 8 * c;
+        for (int k = 0; k < 3; ++k) {
+            o[k] = lo[k];
+            o[3 + k] = hi[k];
+        }
+        o[6] = o[7] = 0.0f;
+    }
+}
+
 }  // namespace
 
 int ef::update_shade(ef_scene* s, cudaStream_t st) {
@@ -95,6 +126,30 @@ int ef::update_shade(ef_scene* s, cudaStream_t st) {
         tribox_kernel<<<(int)((s->n_tri + 255) / 256), 256, 0, st>>>(s->tri_box, s->tris_by_id,
                                                                       s->n_tri, s->pad);
         count_launch();
+        // each triangle once, in (first) leaf order
+        const bool host_order = (int64_t)s->clu_order.size() == s->n_tri;
+        if (host_order || (s->leaf_order && s->n_refs == s->n_tri)) {
+            const int64_t n_clu = (s->n_tri + kTailCluster - 1) / kTailCluster;
+            if (!s->clu_box) {
+                cudaError_t e = cudaMalloc((void**)&s->clu_box, (size_t)n_clu * 8 * sizeof(float));
+                if (e == cudaSuccess) e = cudaMalloc((void**)&s->clu_ids, (size_t)s->n_tri * sizeof(int32_t));
+                if (e != cudaSuccess) return check_cuda(e, "update_shade clusters");
+                s->device_bytes += n_clu * 32 + s->n_tri * 4;
+            }
+            s->n_clu = n_clu;
+            cudaError_t e = cudaSuccess;
+            if (host_order) {
+                e = cudaMemcpyAsync(s->clu_ids, s->clu_order.data(), (size_t)s->n_tri * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, st);
+            } else {
+                order_kernel<<<(int)((s->n_tri + 255) / 256), 256, 0, st>>>(s->clu_ids, s->leaf_order, s->n_tri);
+                count_launch();
+            }
+            if (e != cudaSuccess) return check_cuda(e, "update_shade clusters");
+            cluster_kernel<<<(int)((n_clu + 127) / 128), 128, 0, st>>>(s->clu_box, s->clu_ids, s->tri_box,
+                                                                      s->n_tri, n_clu);
+            count_launch();
+        }
     }
     return check_cuda(cudaGetLastError(), "shade_kernel");
 }
@@ -216,6 +271,14 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
                 mat[t] = (int32_t)material_index[t];
             }
             s->n_refs = n_refs;
+            if (n_tri <= kTailMaxTris) {   // leaf order with repeats dropped (tail sweep clusters)
+                std::vector<char> seen(n_tri, 0);
+                for (int64_t i = 0; i < n_refs; ++i)
+                    if (!seen[bvh.order[i]]) {
+                        seen[bvh.order[i]] = 1;
+                        s->clu_order.push_back((int32_t)bvh.order[i]);
+                    }
+            }
             s->n_nodes = (int64_t)bvh.nodes.size();
             s->max_depth = bvh.max_depth;
             s->max_leaf = bvh.max_leaf;
@@ -372,6 +435,7 @@ extern "C" int ef_scene_rebuild(ef_scene* s, const double* v0, const double* e1,
         s->tris_by_id, s->normals, v0, e1, e2, normals, n);
     count_launch();
     int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
+    s->clu_order.clear();   // the device tree's leaf order from now on
     if (rc == EF_OK) rc = device_build_bvh(s, v0, e1, e2, 3, st);
     if (rc != EF_OK) return rc;
     return update_shade(s, st);   // after the build: the boxes use its padding

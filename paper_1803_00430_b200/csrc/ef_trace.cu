@@ -120,6 +120,9 @@ struct TraceParams {
     int32_t n_tri;
     const GpuShade* shade;
     const float* tri_box;
+    const float* clu_box;       // tail sweep level 1 (n_clu clusters of kTailCluster leaf-order triangles)
+    const int32_t* clu_ids;
+    int32_t n_clu, n_refs;
     const float* fd;
     const float* fs;
     int32_t nb;
@@ -628,7 +631,8 @@ constexpr int kTailThreads = 512;
 // triangle scene); the f64 triangles stay in L1 (staging them instead --
 // 72 B each -- shrinks L1 below the boxes' working set: 3.05 vs 2.44 us per
 // segment on C2).
-constexpr size_t kTailStageBytes = (size_t)kTailMaxTris * 32;
+constexpr size_t kTailStageBytes = (size_t)kTailMaxTris * 32 + (size_t)kTailThreads * 32 +
+                                   (size_t)kTailThreads * kTailCluster * 4;
 
 template <int NBMAX, int ORDER>
 __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams P) {
@@ -639,6 +643,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
     __shared__ double s_ray[6];
     __shared__ int s_active;
     __shared__ unsigned s_j;
+    __shared__ int s_hitc[kTailThreads];   // clusters whose box the ray crosses
+    __shared__ int s_nhit;
     constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const unsigned n_long = min(P.cont_count[0], (unsigned)P.tail_live);
@@ -646,16 +652,23 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
     if (blockIdx.x >= n) return;   // no path for this CTA
     const PathState<NBMAX>* cont = reinterpret_cast<const PathState<NBMAX>*>(P.cont);
     const LaneGroup lg = lane_group<32>();
+    // shared: triangle boxes by id, cluster boxes, leaf-order ids
+    float4* s_cbox = s_box + 2 * P.n_tri;
+    int* s_cid = reinterpret_cast<int*>(s_cbox + 2 * P.n_clu);
     {
         const float4* src = reinterpret_cast<const float4*>(P.tri_box);
 #pragma unroll 4
         for (int k = tid; k < 2 * P.n_tri; k += kTailThreads) s_box[k] = __ldg(src + k);
+        const float4* csrc = reinterpret_cast<const float4*>(P.clu_box);
+        for (int k = tid; k < 2 * P.n_clu; k += kTailThreads) s_cbox[k] = __ldg(csrc + k);
+        for (int k = tid; k < P.n_refs; k += kTailThreads) s_cid[k] = __ldg(P.clu_ids + k);
     }
     const double* tris = P.tris_by_id;
     if (tid == 0) {
         s_tb = kInfBits;
         s_id = INT32_MAX;
         s_nc = 0;
+        s_nhit = 0;
     }
     for (;;) {
         if (tid == 0) s_j = atomicAdd(P.cont_take, 1u);
@@ -676,30 +689,30 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
             // ---- candidates by box, exact test, (t, id) minimum over the CTA
             const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
             const float tminf = fmaxf(__double2float_rd(kRayEps), 0.0f);
-            const float4* box = s_box;
             Hit h{INFINITY, INT32_MAX};
             int nc = 0;
-            for (int i0 = tid; i0 < P.n_tri; i0 += 4 * kTailThreads) {
-                uint32_t cand = 0;   // boxes of four triangles first, all loads in flight
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = i0 + u * kTailThreads;
-                    if (i < P.n_tri) {
-                        const float4 a = box[2 * i], b = box[2 * i + 1];
-                        if (slab_key_minmax(r, a.x, a.w, a.y, b.x, a.z, b.y, tminf, 1e38f, 0u) != 0xffffffffu)
-                            cand |= 1u << u;
-                    }
-                }
-                while (cand) {   // ascending ids: '<' keeps the lowest on equal t
-                    const int u = __ffs(cand) - 1;
-                    cand &= cand - 1u;
-                    const int i = i0 + u * kTailThreads;
-                    ++nc;
-                    double t;
-                    if (mt_hit(ox, oy, oz, dx, dy, dz, tris + 9 * i, kRayEps, INFINITY, t) && t < h.t) {
-                        h.t = t;
-                        h.id = i;
-                    }
+            // level 1: the clusters (unions of 16 leaf-order triangle boxes)
+            for (int c = tid; c < P.n_clu; c += kTailThreads) {
+                const float4 a = s_cbox[2 * c], b = s_cbox[2 * c + 1];
+                if (slab_key_minmax(r, a.x, a.w, a.y, b.x, a.z, b.y, tminf, 1e38f, 0u) != 0xffffffffu)
+                    s_hitc[atomicAdd(&s_nhit, 1)] = c;
+            }
+            __syncthreads();
+            // level 2: the triangles of the crossed clusters, one per thread
+            const int nh = s_nhit;
+            for (int q = tid; q < nh * kTailCluster; q += kTailThreads) {
+                const int ref = s_hitc[q / kTailCluster] * kTailCluster + q % kTailCluster;
+                if (ref >= P.n_refs) continue;
+                const int i = s_cid[ref];
+                const float4 a = s_box[2 * i], b = s_box[2 * i + 1];
+                if (slab_key_minmax(r, a.x, a.w, a.y, b.x, a.z, b.y, tminf, 1e38f, 0u) == 0xffffffffu)
+                    continue;
+                ++nc;
+                double t;   // any order: (t, id) compared lexicographically
+                if (mt_hit(ox, oy, oz, dx, dy, dz, tris + 9 * i, kRayEps, INFINITY, t) &&
+                    (t < h.t || (t == h.t && i < h.id))) {
+                    h.t = t;
+                    h.id = i;
                 }
             }
 #ifdef EF_PROFILE_PHASES
@@ -733,6 +746,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
                     s_tb = kInfBits;
                     s_id = INT32_MAX;
                     s_nc = 0;
+                    s_nhit = 0;
                 }
             }
 #ifdef EF_PROFILE_PHASES
@@ -847,7 +861,8 @@ static cudaError_t launch_tail_o(const TraceParams& P, cudaStream_t st) {
         attr_done = true;
     }
     const int grid = (int)std::max(1, std::min(P.tail_live, sm_count()));
-    const size_t smem = (size_t)P.n_tri * 32;   // n_tri <= kTailMaxTris (tail_live == 0 otherwise)
+    // n_tri <= kTailMaxTris, n_clu <= kTailThreads (tail_live == 0 otherwise)
+    const size_t smem = (size_t)P.n_tri * 32 + (size_t)P.n_clu * 32 + (size_t)P.n_refs * 4;
     tail_kernel<NBMAX, ORDER><<<grid, kTailThreads, smem, st>>>(P);
     count_launch();
     return cudaGetLastError();
@@ -1113,7 +1128,8 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         const char* v = std::getenv("EF_TAIL_LIVE");
         return v ? std::atoi(v) : -1;
     }();
-    const int tail_live = (brute || s->n_tri > kTailMaxTris || !s->tri_box) ? 0
+    const int tail_live = (brute || s->n_tri > kTailMaxTris || !s->tri_box || !s->clu_box ||
+                           s->n_clu > kTailThreads) ? 0
                           : (tail_env >= 0 ? tail_env : 2 * sm_count());
     // scratch header: path counter (u64), finished paths (u64), continuation
     // counts (u32 long, u32 short), entries taken (u32); then the list
@@ -1134,6 +1150,10 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         P.n_tri = (int32_t)s->n_tri;
         P.shade = s->shade;
         P.tri_box = s->tri_box;
+        P.clu_box = s->clu_box;
+        P.clu_ids = s->clu_ids;
+        P.n_clu = (int32_t)s->n_clu;
+        P.n_refs = (int32_t)s->n_tri;   // ids in clu_ids: each triangle once
         P.fd = s->fd;
         P.fs = s->fs;
         P.nb = s->n_bands;
