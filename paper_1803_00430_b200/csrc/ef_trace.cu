@@ -285,6 +285,15 @@ __device__ __forceinline__ LaneGroup lane_group() {
     return g;
 }
 
+// The parts of a segment that do not depend on its hit, computed ahead by
+// the tail kernel's warp 0 while the other warps sweep: the listener test's
+// dot products and this lane's Philox draw for the reflection (same
+// expressions as finish_segment's, so the same bits).
+struct SegPre {
+    double tc, dist2;
+    uint4 xg;
+};
+
 // The rest of a segment once its closest hit h is known: listener sphere and
 // SH histogram commit -> reflection.  With G > 1 the
 // group's lanes split the Philox draws (and diffuse-rain shadow rays on the
@@ -292,7 +301,7 @@ __device__ __forceinline__ LaneGroup lane_group() {
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
 __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                                const Hit h, const double* s_tri, uint2* s_stack,
-                                               const LaneGroup& lg);
+                                               const LaneGroup& lg, const SegPre* pre = nullptr);
 
 // One segment of an active path: closest hit, then finish_segment.  With
 // G > 1 the group's lanes split the closest hit's triangle tests.
@@ -322,7 +331,7 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
 __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                                const Hit h, const double* s_tri, uint2* s_stack,
-                                               const LaneGroup& lg) {
+                                               const LaneGroup& lg, const SegPre* pre) {
     const int nb = P.nb;
     const int gl = lg.gl;
     const bool lead = lg.lead;
@@ -335,10 +344,10 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
     // through the next-event connection: SPEC.md:257, no double count)
     if (!(P.rain && S.last_diffuse)) {
         const double Lx = P.lx - S.ox, Ly = P.ly - S.oy, Lz = P.lz - S.oz;
-        const double tc = dot3(Lx, Ly, Lz, S.dx, S.dy, S.dz);
+        const double tc = pre ? pre->tc : dot3(Lx, Ly, Lz, S.dx, S.dy, S.dz);
         const double tlim = hit ? h.t : INFINITY;
         if (tc > 0.0 && tc < tlim) {
-            const double dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
+            const double dist2 = pre ? pre->dist2 : dot3(Lx, Ly, Lz, Lx, Ly, Lz);
             const double perp2 = dist2 - tc * tc;
             if (perp2 <= P.r2 && lead)
                 commit_arrival<NBMAX, ORDER>(P, S.src, S.nrefl, S.tri0, S.tri1, S.plen + tc, -S.dx,
@@ -375,8 +384,9 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         uint4 xg;   // lane groups: this lane's draw (ray, bounce, gl) -- all of a
                     // group's draws come from one Philox latency instead of a chain
         if (G > 1) {
-            xg = philox(make_uint4(S.ray, (uint32_t)S.nrefl, (uint32_t)gl, P.frame),
-                        make_uint2(P.seed, S.skey));
+            xg = pre ? pre->xg
+                     : philox(make_uint4(S.ray, (uint32_t)S.nrefl, (uint32_t)gl, P.frame),
+                              make_uint2(P.seed, S.skey));
             u1 = u53(__shfl_sync(lg.gmask, xg.x, 0, G), __shfl_sync(lg.gmask, xg.y, 0, G));
         } else {
             draw2(S.ray, (uint32_t)S.nrefl, 0u, P.frame, P.seed, S.skey, u1, u2);
@@ -691,8 +701,20 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
             const float tminf = fmaxf(__double2float_rd(kRayEps), 0.0f);
             Hit h{INFINITY, INT32_MAX};
             int nc = 0;
+            // warp 0: the hit-independent part of finish_segment; warps 1..15:
+            // the sweep
+            SegPre pre;
+            if (w == 0) {
+                const double Lx = P.lx - S.ox, Ly = P.ly - S.oy, Lz = P.lz - S.oz;
+                pre.tc = dot3(Lx, Ly, Lz, S.dx, S.dy, S.dz);
+                pre.dist2 = dot3(Lx, Ly, Lz, Lx, Ly, Lz);
+                pre.xg = philox(make_uint4(S.ray, (uint32_t)(S.nrefl + 1), (uint32_t)lane, P.frame),
+                                make_uint2(P.seed, S.skey));
+            }
+            constexpr int kSweep = kTailThreads - 32;
+            const int st = tid - 32;   // sweep thread index (warp 0: none)
             // level 1: the clusters (unions of 16 leaf-order triangle boxes)
-            for (int c = tid; c < P.n_clu; c += kTailThreads) {
+            for (int c = st; c >= 0 && c < P.n_clu; c += kSweep) {
                 const float4 a = s_cbox[2 * c], b = s_cbox[2 * c + 1];
                 if (slab_key_minmax(r, a.x, a.w, a.y, b.x, a.z, b.y, tminf, 1e38f, 0u) != 0xffffffffu)
                     s_hitc[atomicAdd(&s_nhit, 1)] = c;
@@ -700,7 +722,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
             __syncthreads();
             // level 2: the triangles of the crossed clusters, one per thread
             const int nh = s_nhit;
-            for (int q = tid; q < nh * kTailCluster; q += kTailThreads) {
+            for (int q = st; q >= 0 && q < nh * kTailCluster; q += kSweep) {
                 const int ref = s_hitc[q / kTailCluster] * kTailCluster + q % kTailCluster;
                 if (ref >= P.n_refs) continue;
                 const int i = s_cid[ref];
@@ -738,7 +760,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
                     h.id = INT32_MAX;
                 }
                 ls.c[EF_ST_TRIS] += (uint32_t)s_nc;
-                finish_segment<NBMAX, ORDER, false, kTailThreads, 32, false>(P, S, ls, h, nullptr, nullptr, lg);
+                finish_segment<NBMAX, ORDER, false, kTailThreads, 32, false>(P, S, ls, h, nullptr, nullptr, lg,
+                                                                             &pre);
                 if (lane == 0) {
                     s_ray[0] = S.ox; s_ray[1] = S.oy; s_ray[2] = S.oz;
                     s_ray[3] = S.dx; s_ray[4] = S.dy; s_ray[5] = S.dz;
