@@ -627,14 +627,16 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
 }
 
 // Tail of a frame (scenes of <= kTailMaxTris triangles): the paths handed off
-// by trace_kernel run one per CTA.  Every segment's closest hit is the
-// all-pairs answer (lowest id on equal t -- the same hit as the BVH's,
-// DESIGN.md 3.2) split over the CTA's 512 threads: an f32 slab test of each
-// triangle's padded box (conservative like the BVH's leaf boxes) picks the
-// candidates, the exact f64 test decides, and a (t, id) reduction joins the
-// threads; warp 0 then finishes the segment as a 32-lane group (parallel
-// draws).  A lone path's segment latency drops from a serial BVH walk (~3.1
-// us on C2) to one CTA-wide sweep.
+// by trace_kernel run one per CTA, long ones first.  Every segment's closest
+// hit is the all-pairs answer (lowest id on equal t -- the same hit as the
+// BVH's) split over warps 1-15: f32 slab tests of cluster
+// boxes (16 leaf-order triangles each), then of the crossed clusters'
+// triangle boxes (all padded and rounded outward like the BVH's leaf boxes,
+// so conservative) pick the candidates, the exact f64 test decides, and two
+// shared-memory atomics reduce (t, id).  Warp 0 meanwhile computes the
+// segment's hit-independent work and then finishes it as a 32-lane group
+// (parallel draws).  A lone path's segment drops from a serial BVH walk
+// (~3.2 us on C2) to ~2.0 us.
 constexpr int kTailThreads = 512;
 
 // Triangle boxes staged in shared memory (32 B each, all of a <= 4,096-
