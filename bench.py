@@ -385,11 +385,14 @@ def run_gpu(args, w, metric, unit):
     bseg = b_seg(args.config, sc.n_bands, nk)
     avg_k_s = (k_ms * 1e-3) / args.steps
     achieved = bseg * segs_per_step / avg_k_s / 1e9
+    # DRAM bytes of the trace call from the committed ncu captures: the trace
+    # kernel plus, where the scene has one, the frame's tail kernel
     traffic = None
-    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+    for suffix in ("", "tail"):
+        tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}{suffix}.json")
+        if os.path.exists(tf):
+            with open(tf) as f:
+                traffic = (traffic or 0.0) + json.load(f).get("dram_bytes_per_launch")
     if world > 1:
         if fused:
             peers.close()
@@ -407,7 +410,8 @@ def run_gpu(args, w, metric, unit):
             "gpu_launches": int(n_launch),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "trace_kernel", "kernel_ms_per_launch": avg_k_s * 1e3,
+                         "kernel": "trace_kernel" + (" + tail_kernel" if 512 < sc.n_triangles <= 4096 else ""),
+                         "kernel_ms_per_launch": avg_k_s * 1e3,
                          "algorithmic_bytes_per_segment": bseg,
                          "segments_per_launch": round(segs_per_step)},
             "step_ms_quantiles": {q: float(np.percentile(step_ms, p)) for q, p in
