@@ -1137,12 +1137,25 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         // DMA-engine clears, no kernel launch
         // (fused: the peer blocks belong to their owners, only local outputs)
         const size_t nh = (size_t)cfg->n_sources * cfg->n_bins * s->n_bands * nk;
-        if (!fused) {
-            e = cudaMemsetAsync(H, 0, nh * sizeof(float), st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(Dir, 0, (size_t)cfg->n_sources * s->n_bands * nk * sizeof(float), st);
+        const size_t nd = (size_t)cfg->n_sources * s->n_bands * nk;
+        const size_t nst = (size_t)cfg->n_sources * EF_ST_COUNT * 8;
+        const char* h0 = reinterpret_cast<const char*>(H);
+        // H | Dir | stats | sum_t back to back (FrameTracer's single
+        // allocation; stats 8-byte aligned right after Dir): one memset
+        const bool packed = !fused && (4 * (nh + nd)) % 8 == 0 &&
+                            reinterpret_cast<const char*>(Dir) == h0 + 4 * nh &&
+                            reinterpret_cast<const char*>(stats) == h0 + 4 * (nh + nd) &&
+                            reinterpret_cast<const char*>(sum_t) == h0 + 4 * (nh + nd) + nst;
+        if (packed) {
+            e = cudaMemsetAsync(H, 0, 4 * (nh + nd) + nst + (size_t)cfg->n_sources * 8, st);
+        } else {
+            if (!fused) {
+                e = cudaMemsetAsync(H, 0, nh * sizeof(float), st);
+                if (e == cudaSuccess) e = cudaMemsetAsync(Dir, 0, nd * sizeof(float), st);
+            }
+            if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, nst, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
         }
-        if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, (size_t)cfg->n_sources * EF_ST_COUNT * 8, st);
-        if (e == cudaSuccess) e = cudaMemsetAsync(sum_t, 0, (size_t)cfg->n_sources * 8, st);
         if (e != cudaSuccess) return check_cuda(e, "cudaMemsetAsync");
     }
     // tail hand-off for small BVH scenes (tail_kernel): at most two paths

@@ -232,10 +232,18 @@ class FrameTracer:
         self.n_sources = n_sources
         self.nb = scene.n_bands
         self.nk = config.n_coeffs
-        self.H = t.zeros((n_sources, config.n_bins, self.nb, self.nk), dtype=t.float32, device=dev)
-        self.Dir = t.zeros((n_sources, self.nb, self.nk), dtype=t.float32, device=dev)
-        self.stats = t.zeros((n_sources, _lib.EF_ST_COUNT), dtype=t.int64, device=dev)
-        self.sum_t = t.zeros((n_sources,), dtype=t.float64, device=dev)
+        # H | Dir | stats | sum_t in one allocation, in that order: ef_trace
+        # then clears a frame's outputs with one memset instead of four
+        nh = n_sources * config.n_bins * self.nb * self.nk
+        nd = n_sources * self.nb * self.nk
+        o_st = -(-4 * (nh + nd) // 8) * 8
+        o_su = o_st + 8 * n_sources * _lib.EF_ST_COUNT
+        self._outputs = t.zeros(o_su + 8 * n_sources, dtype=t.uint8, device=dev)
+        buf = self._outputs
+        self.H = buf[:4 * nh].view(t.float32).view(n_sources, config.n_bins, self.nb, self.nk)
+        self.Dir = buf[4 * nh:4 * (nh + nd)].view(t.float32).view(n_sources, self.nb, self.nk)
+        self.stats = buf[o_st:o_su].view(t.int64).view(n_sources, _lib.EF_ST_COUNT)
+        self.sum_t = buf[o_su:].view(t.float64)
         self.src_pos = t.zeros((n_sources, 3), dtype=t.float64, device=dev)
         self.src_key = t.arange(n_sources, dtype=t.int32, device=dev)
         self.record = record
