@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kKThreads) analyze_kernel(const AnalyzeParams 
         for (int k = 0; k < NK; ++k) s_B[j * NK + k] = Y[k];
     }
     if (tid == 0) s_dblast = 0.0;
+    pdl_wait();   // the design table above is ready; H is final from here
 
 #ifdef EF_PROFILE_PHASES
     const long long a0 = clock64();   // analysis phases (counters of the analysis TU)
@@ -539,14 +540,27 @@ extern "C" int ef_analyze(const ef_analysis_config* cfg, const float* H, const f
         analyze_set_smem<3>(); analyze_set_smem<4>();
         attr_done = true;
     }
+    // PDL: the kernel may be scheduled before the trace (or tail) kernel ends;
+    // it evaluates its t-design table, then waits for the histograms
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t le = cudaSuccess;
     switch (cfg->order) {
-        case 0: analyze_kernel<0><<<grid, block, smem, st>>>(P); break;
-        case 1: analyze_kernel<1><<<grid, block, smem, st>>>(P); break;
-        case 2: analyze_kernel<2><<<grid, block, smem, st>>>(P); break;
-        case 3: analyze_kernel<3><<<grid, block, smem, st>>>(P); break;
-        default: analyze_kernel<4><<<grid, block, smem, st>>>(P); break;
+        case 0: le = cudaLaunchKernelEx(&lc, analyze_kernel<0>, P); break;
+        case 1: le = cudaLaunchKernelEx(&lc, analyze_kernel<1>, P); break;
+        case 2: le = cudaLaunchKernelEx(&lc, analyze_kernel<2>, P); break;
+        case 3: le = cudaLaunchKernelEx(&lc, analyze_kernel<3>, P); break;
+        default: le = cudaLaunchKernelEx(&lc, analyze_kernel<4>, P); break;
     }
-    cudaError_t le = cudaGetLastError();
+    if (le == cudaSuccess) le = cudaGetLastError();
     count_launch();
     return check_cuda(le, "analyze_kernel");
 }

@@ -21,6 +21,15 @@ static __device__ unsigned long long g_phase[12];   // per translation unit
 #define EF_PHASE_ADD(i, v)
 #endif
 
+// ------------------------------------------------ dependent launches ----
+// Programmatic dependent launch (PDL): a kernel lets the next kernel on its
+// stream be scheduled before it ends (pdl_trigger); the next kernel runs its
+// input-independent prologue, then pdl_wait() blocks until this grid has
+// completed and its memory is visible.  Both are no-ops without the launch
+// attribute (launch_pdl in ef_trace.cu / ef_analyze.cu).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- RNG ----
 // Philox4x32-10 (Salmon et al. 2011); key = (seed, source key),
 // counter = (ray, bounce, draw, frame).  DESIGN.md 3.1.

@@ -512,6 +512,7 @@ template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK 
 __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) {
     static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
     static_assert(G == 1 || BRUTE, "lane groups are for the all-pairs path");
+    pdl_trigger();   // the tail / analysis kernel may be scheduled onto SMs this grid frees
     extern __shared__ __align__(16) unsigned char smem[];
     // per-block counters: f64 path-length sums, then u32 counters (a block's
     // per-source counts stay far below 2^32), then the all-pairs triangles
@@ -659,9 +660,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
     __shared__ int s_nhit;
     constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const unsigned n_long = min(P.cont_count[0], (unsigned)P.tail_live);
-    const unsigned n = min(n_long + P.cont_count[1], (unsigned)P.tail_live);
-    if (blockIdx.x >= n) return;   // no path for this CTA
+    pdl_trigger();
     const PathState<NBMAX>* cont = reinterpret_cast<const PathState<NBMAX>*>(P.cont);
     const LaneGroup lg = lane_group<32>();
     // shared: triangle boxes by id, cluster boxes, leaf-order ids
@@ -675,6 +674,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
         for (int k = tid; k < 2 * P.n_clu; k += kTailThreads) s_cbox[k] = __ldg(csrc + k);
         for (int k = tid; k < P.n_refs; k += kTailThreads) s_cid[k] = __ldg(P.clu_ids + k);
     }
+    pdl_wait();   // (staged while the trace kernel drained) its hand-offs are final from here
+    const unsigned n_long = min(P.cont_count[0], (unsigned)P.tail_live);
+    const unsigned n = min(n_long + P.cont_count[1], (unsigned)P.tail_live);
+    if (blockIdx.x >= n) return;   // no path for this CTA
     const double* tris = P.tris_by_id;
     if (tid == 0) {
         s_tb = kInfBits;
@@ -888,9 +891,19 @@ static cudaError_t launch_tail_o(const TraceParams& P, cudaStream_t st) {
     const int grid = (int)std::max(1, std::min(P.tail_live, sm_count()));
     // n_tri <= kTailMaxTris, n_clu <= kTailThreads (tail_live == 0 otherwise)
     const size_t smem = (size_t)P.n_tri * 32 + (size_t)P.n_clu * 32 + (size_t)P.n_refs * 4;
-    tail_kernel<NBMAX, ORDER><<<grid, kTailThreads, smem, st>>>(P);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kTailThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after trace_kernel
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&lc, tail_kernel<NBMAX, ORDER>, P);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int NBMAX>
