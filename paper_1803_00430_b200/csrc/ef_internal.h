@@ -16,7 +16,10 @@ constexpr double kRayEps = 1e-4;     // scene.py:22
 constexpr int kStackSize = 96;
 constexpr int kMaxLeaf = 4;
 constexpr int kTailMaxTris = 4096;   // scenes small enough for the CTA-wide tail sweep
-constexpr int kTailCluster = 16;     // leaf-order triangles per tail-sweep cluster
+#ifndef EF_TAIL_CLUSTER
+#define EF_TAIL_CLUSTER 16
+#endif
+constexpr int kTailCluster = EF_TAIL_CLUSTER;   // leaf-order triangles per tail-sweep cluster
 
 // Four-child BVH node, 128 bytes = eight 16-byte vectors, child boxes in
 // structure-of-arrays form so one node visit is 7 vector loads and four

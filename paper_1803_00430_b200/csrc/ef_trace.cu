@@ -638,7 +638,10 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
 // segment's hit-independent work and then finishes it as a 32-lane group
 // (parallel draws).  A lone path's segment drops from a serial BVH walk
 // (~3.2 us on C2) to ~2.0 us.
-constexpr int kTailThreads = 512;
+#ifndef EF_TAIL_THREADS
+#define EF_TAIL_THREADS 512
+#endif
+constexpr int kTailThreads = EF_TAIL_THREADS;   // (tuning builds may override)
 
 // Triangle boxes staged in shared memory (32 B each, all of a <= 4,096-
 // triangle scene); the f64 triangles stay in L1 (staging them instead --
