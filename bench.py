@@ -313,6 +313,7 @@ def run_gpu(args, w, metric, unit):
         step()
     torch.cuda.synchronize()
     arrivals = int(tr.stats[:, 3].sum().item())
+    tail_segs = int(tr.stats[:, 9].sum().item())   # of the last warm-up frame (EF_ST_TAIL)
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -417,6 +418,7 @@ def run_gpu(args, w, metric, unit):
             "step_ms_quantiles": {q: float(np.percentile(step_ms, p)) for q, p in
                                   (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))},
             "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
+            "tail_segments_per_step": tail_segs,
             "clocks": clocks.summary()}
     if exchange_note:
         line["exchange_note"] = exchange_note

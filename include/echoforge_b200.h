@@ -53,6 +53,8 @@ enum {
     EF_ST_ESCAPED,         /* paths that left the scene                         */
     EF_ST_NODES,           /* BVH nodes visited (device tree)                   */
     EF_ST_TRIS,            /* exact triangle tests (device tree / all-pairs)    */
+    EF_ST_TAIL,            /* segments run by the frame-tail kernel (subset of  */
+                           /* EF_ST_SEGMENTS; scenes of 513-4,096 triangles)    */
     EF_ST_COUNT = 10
 };
 

@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TraceParams
                     h.id = INT32_MAX;
                 }
                 ls.c[EF_ST_TRIS] += (uint32_t)s_nc;
+                ls.c[EF_ST_TAIL]++;
                 finish_segment<NBMAX, ORDER, false, kTailThreads, 32, false>(P, S, ls, h, nullptr, nullptr, lg,
                                                                              &pre);
                 if (lane == 0) {

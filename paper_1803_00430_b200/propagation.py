@@ -92,6 +92,7 @@ class TraceStats:
     open_field: bool = False
     nodes_visited: int = 0        # device BVH work (not the reference's)
     triangles_tested: int = 0
+    tail_segments: int = 0        # segments run by the frame-tail kernel
 
 
 @dataclass
@@ -211,11 +212,12 @@ class CoherenceCaches:
 
 
 def _stats_from_row(row: np.ndarray, sum_t: float) -> TraceStats:
-    paths, segs, refl, arr, direct, dropped, esc, nodes, tris = (int(x) for x in row[:9])
+    paths, segs, refl, arr, direct, dropped, esc, nodes, tris, tail = (int(x) for x in row[:10])
     return TraceStats(mean_free_path=sum_t / refl if refl else 0.0,
                       primary_rays_emitted=paths, total_segments=segs, reflections=refl,
                       arrivals=arr, direct_arrivals=direct, dropped_late=dropped, escaped=esc,
-                      open_field=refl == 0, nodes_visited=nodes, triangles_tested=tris)
+                      open_field=refl == 0, nodes_visited=nodes, triangles_tested=tris,
+                      tail_segments=tail)
 
 
 class FrameTracer:
