@@ -2,20 +2,25 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
 
-One step = one frame of the configured workload (default C2, BASELINE.json
-configs[1]: 2,402-triangle procedural city, 8 sources x 32,768 paths, 100
-bounces, order-3 SH histogram, 4 bands): ef_trace (one persistent kernel
-over all paths of all sources, histogram cleared by DMA first) followed by
-ef_analyze (per-band RT60/DRR/predelay/loudness).  N > 1 (torchrun): weak
-scaling, every rank traces its own 32,768-ray slice of every source
-(global ray index = rank * R + i) and the partial histograms are summed with
-one NCCL reduce-scatter per frame, each rank then analysing S/N sources.
+One step = one frame of the configured workload (default C5, BASELINE.json
+configs[4], the largest config that fits one B200: 964,002-triangle city
+grid, 256 sources x 2^20 paths, 100 bounces, 8 bands, order-3 SH histogram):
+ef_trace (one persistent kernel over all paths of all sources, histogram
+cleared by DMA first) followed by ef_analyze (per-band RT60/DRR/predelay/
+loudness).  N > 1 (torchrun): strong scaling, the frame is fixed and rank g
+traces rays [g*R/N, (g+1)*R/N) of every source (global Philox ray indices,
+so the paths are those of the 1-GPU frame); the splats go straight to the
+owning rank's histogram blocks inside the trace kernel (ef_trace_fused) or,
+with --exchange nccl, one reduce-scatter per frame; each rank then analyses
+its S/N sources.
 
 Timing: CUDA events per step on the launching stream, L2 flushed (256 MiB
 write) between steps outside the events, max over ranks.  ``e2e`` repeats
 the steps through the public API with the source positions copied in from
-pinned host memory and the frame's result (reverb parameters per source and
-band) copied back, both inside the timed region.  ``--impl reference`` times the CPU oracle
+pinned host memory and the frame's result -- the LowRateIR histograms and
+direct blocks of the rank's sources (what trace_frame returns)
+and the reverb parameters per source and band -- copied back to pinned host
+memory, all inside the timed region.  ``--impl reference`` times the CPU oracle
 port of the reference algorithm (oracle/efo.c, every host core) instead.
 """
 from __future__ import annotations
@@ -184,7 +189,7 @@ def run_reference(args, w, metric, unit):
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(args, w, world),
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
                              "sample": sample},
@@ -197,9 +202,10 @@ def config_block(args, w, world, exchange=None):
     exchange = exchange or args.exchange
     return {"workload": f"{w.name} (BASELINE.json configs[{ {'c1': 0, 'c2': 1, 'c3': 2, 'c5': 4}[args.config] }])",
             "triangles": int(w.n_tri), "sources": int(len(w.sources)),
-            "rays_per_source_per_rank": int(w.n_rays), "max_bounces": int(w.max_bounces),
+            "rays_per_source": int(w.n_rays), "rays_per_source_per_rank": int(w.n_rays // world),
+            "max_bounces": int(w.max_bounces),
             "sh_order": int(w.order), "bands": int(w.n_bands), "bins": int(w.n_bins),
-            "parallelism": (f"rays sharded x{world}, " + (
+            "parallelism": (f"each source's rays sharded x{world} (fixed frame), " + (
                 "histograms reduce-scattered inside the trace kernel (ef_trace_fused, peer memory)"
                 if exchange == "fused" else "NCCL reduce-scatter of histograms")) if world > 1
             else "single GPU", "l2": "flushed between steps (256 MiB write)"}
@@ -253,8 +259,13 @@ def run_gpu(args, w, metric, unit):
         su_own = torch.empty((S_own,), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    total_rays = w.n_rays * world
-    ray0 = rank * w.n_rays
+    # strong scaling: the frame is fixed; rank g traces rays [g*R/N, (g+1)*R/N)
+    # of every source (global Philox ray index, e0 normalised by R)
+    if w.n_rays % world:
+        raise SystemExit("rays per source must divide by the number of ranks")
+    total_rays = w.n_rays
+    n_rays = w.n_rays // world
+    ray0 = rank * n_rays
     # C3: moving sources, temporal IR cache (accumulate_ir, tau_LR = 3 s) and
     # per-frame estimation on the cached IR
     dynamic = w.n_frames > 1 and w.source_velocity is not None
@@ -267,6 +278,8 @@ def run_gpu(args, w, metric, unit):
         H_cache = torch.zeros((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
         D_cache = torch.zeros((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
     seg_total = torch.zeros((), dtype=torch.int64, device=dev)
+    tail_total = torch.zeros((), dtype=torch.int64, device=dev)
+    work_total = torch.zeros(3, dtype=torch.int64, device=dev)   # nodes, triangles, arrivals
     counter = [0]
 
     def step(kernel_events=None):
@@ -279,9 +292,10 @@ def run_gpu(args, w, metric, unit):
             kernel_events[0].record(stream)
         if fused:
             peers.begin_frame(seq)
-            tr.trace_fused(w.listener, peers, frame=f, ray0=ray0, total_rays=total_rays, slot=seq)
+            tr.trace_fused(w.listener, peers, frame=f, ray0=ray0, n_rays=n_rays, total_rays=total_rays,
+                           slot=seq)
         else:
-            tr.trace(w.listener, frame=f, ray0=ray0, total_rays=total_rays)
+            tr.trace(w.listener, frame=f, ray0=ray0, n_rays=n_rays, total_rays=total_rays)
         if kernel_events:
             kernel_events[1].record(stream)
         if fused:
@@ -308,12 +322,11 @@ def run_gpu(args, w, metric, unit):
             blend_into(D_cache, ds, alpha)
             hs, ds = H_cache, D_cache
         an.run(hs, ds, sts, sus)
+        return hs, ds
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    arrivals = int(tr.stats[:, 3].sum().item())
-    tail_segs = int(tr.stats[:, 9].sum().item())   # of the last warm-up frame (EF_ST_TAIL)
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -330,6 +343,8 @@ def run_gpu(args, w, metric, unit):
             step(kev[i])
             ends[i].record(stream)
             seg_total.add_(tr.stats[:, 1].sum())     # after the end event: not timed
+            tail_total.add_(tr.stats[:, 9].sum())    # EF_ST_TAIL
+            work_total.add_(tr.stats[:, [7, 8, 3]].sum(0))
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -338,12 +353,18 @@ def run_gpu(args, w, metric, unit):
     ms = sum(step_ms)
     k_ms = sum(a.elapsed_time(b) for a, b in kev)
     segs_per_step = int(seg_total.item()) / args.steps   # this rank's mean segments per frame
+    tail_segs = int(tail_total.item()) / args.steps
+    nodes_step, tris_step, arr_step = (int(x) / args.steps for x in work_total.cpu())
+    arrivals = arr_step
 
     # ---- e2e through the public API: pinned host in/out, copies timed
     src_host = torch.from_numpy(np.ascontiguousarray(w.sources, np.float64)).pin_memory()
-    # the step's result is the per-(source, band) reverb parameters and the
-    # per-source predelay / mean free path (the IR itself stays on the device,
-    # where the next frame's temporal cache and the renderer consume it)
+    # the step's result: the LowRateIR (histogram + direct block) of each of
+    # this rank's sources -- what trace_frame returns --
+    # plus the per-(source, band) reverb parameters and per-source predelay /
+    # mean free path
+    H_host = torch.empty((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32).pin_memory()
+    D_host = torch.empty((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32).pin_memory()
     P_host = torch.empty(tuple(an.params.shape), dtype=torch.float64).pin_memory()
     Q_host = torch.empty(tuple(an.src_params.shape), dtype=torch.float64).pin_memory()
     e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -351,7 +372,9 @@ def run_gpu(args, w, metric, unit):
 
     def e2e_step():
         tr.src_pos.copy_(src_host, non_blocking=True)
-        step()
+        hs, ds = step()
+        H_host.copy_(hs, non_blocking=True)
+        D_host.copy_(ds, non_blocking=True)
         P_host.copy_(an.params, non_blocking=True)
         Q_host.copy_(an.src_params, non_blocking=True)
 
@@ -368,7 +391,7 @@ def run_gpu(args, w, metric, unit):
     torch.cuda.synchronize()
     e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
     h2d = src_host.numel() * 8
-    d2h = P_host.numel() * 8 + Q_host.numel() * 8
+    d2h = H_host.numel() * 4 + D_host.numel() * 4 + P_host.numel() * 8 + Q_host.numel() * 8
 
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, k_ms, e_ms], dtype=torch.float64, device=dev)
@@ -401,9 +424,30 @@ def run_gpu(args, w, metric, unit):
         dist.destroy_process_group()   # every rank tears NCCL down before exit
     if rank != 0:
         return
+    # device-work roofline: the bytes the device kernels themselves touch per
+    # segment (their own counters: 128-byte 4-wide nodes visited, 80-byte
+    # triangle records tested, one 48-byte shading record + two f32 factor
+    # rows per segment, a histogram read-modify-write per arrival), against
+    # the measured L2 bandwidth (tools/micro/cache_bw.cu,
+    # profiles/micro_peaks.json): the working set is L1/L2-resident
+    dev_bytes = (128.0 * nodes_step + 80.0 * tris_step + (48 + 8 * sc.n_bands) * segs_per_step
+                 + arr_step * 8 * sc.n_bands * nk)
+    micro = {}
+    mp = os.path.join(ROOT, "profiles", "micro_peaks.json")
+    if os.path.exists(mp):
+        with open(mp) as f:
+            micro = json.load(f)
+    dev_achieved = dev_bytes / avg_k_s / 1e9
+    roof_dev = {"bound": "l2", "achieved": dev_achieved, "unit": "GB/s",
+                "peak": micro.get("l2_read_gbs"), "l1_peak": micro.get("l1_read_gbs"),
+                "frac": dev_achieved / micro["l2_read_gbs"] if micro.get("l2_read_gbs") else None,
+                "bytes_per_segment": dev_bytes / max(segs_per_step, 1.0),
+                "nodes_per_segment": nodes_step / max(segs_per_step, 1.0),
+                "triangles_per_segment": tris_step / max(segs_per_step, 1.0),
+                "peak_source": "profiles/micro_peaks.json (tools/micro/cache_bw.cu)" if micro else None}
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(args, w, world, "fused" if fused else "nccl"),
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / args.steps,
@@ -417,6 +461,7 @@ def run_gpu(args, w, metric, unit):
                          "segments_per_launch": round(segs_per_step)},
             "step_ms_quantiles": {q: float(np.percentile(step_ms, p)) for q, p in
                                   (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))},
+            "roofline_device": roof_dev,
             "segments_per_step": total_segs / args.steps, "arrivals_per_step": arrivals,
             "tail_segments_per_step": tail_segs,
             "clocks": clocks.summary()}
@@ -593,9 +638,9 @@ def run_c4(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(WORK) + ["c4"])
+    ap.add_argument("--steps", type=int, default=None, help="default 10 (C5), 200 (others)")
+    ap.add_argument("--warmup", type=int, default=None, help="default 3 (C5), 10 (others)")
+    ap.add_argument("--config", default="c5", choices=sorted(WORK) + ["c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-fraction", type=float, default=None,
                     help="fraction of each source's rays in the CPU sample (default per config)")
@@ -608,6 +653,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum wall time of the CPU baseline sample")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if args.config == "c5" else 200
+    if args.warmup is None:
+        args.warmup = 3 if args.config == "c5" else 10
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1803_00430_b200 import workloads
     if args.config == "c4":

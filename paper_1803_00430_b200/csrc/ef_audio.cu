@@ -195,6 +195,9 @@ __device__ __forceinline__ Window window(int start, int L) {
 // Producer lane: arm stage barrier `bar` with the job's byte count, then
 // issue the bulk copies of job (s, b) into stage `buf`: the 16 line windows
 // (off[i] = window start in line i), the band's line -> SH matrix and gains.
+// The offsets are stored BEFORE the arrive.expect_tx: that arrive releases
+// the lane's earlier shared-memory writes to the consumers that pass the
+// stage's full barrier (complete_tx only publishes the copied bytes).
 __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, float* buf, int* off,
                                           uint32_t bar) {
     const int L = A.line_len;
@@ -205,6 +208,7 @@ __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, flo
         start[i] = (int)((A.t - __ldg(A.m + s * kLines + i)) & (L - 1));
         const Window w = window(start[i], L);
         bytes += (uint32_t)(w.n1 + w.n2) * 4u;
+        off[i] = start[i] - w.a0;
     }
     mbar_expect_tx(bar, bytes);
     const size_t sb = (size_t)s * kBands + b;
@@ -215,7 +219,6 @@ __device__ __forceinline__ void issue_job(const AudioState& A, int s, int b, flo
         const Window w = window(start[i], L);
         const float* row = A.lines + (((size_t)s * kBands + b) * kLines + i) * L;
         const uint32_t dst = smem_addr(buf + i * kWin);
-        off[i] = start[i] - w.a0;
         bulk_g2s(dst, row + w.a0, (uint32_t)w.n1 * 4u, bar);
         if (w.n2) bulk_g2s(dst + (uint32_t)w.n1 * 4u, row, (uint32_t)w.n2 * 4u, bar);
     }

@@ -177,6 +177,31 @@ __device__ __forceinline__ bool mt_full(double ox, double oy, double oz, double 
     return ok && (u >= -1e-10) && (vv >= -1e-10) && (u + vv <= 1.0 + 1e-10);
 }
 
+// ------------------------------------------------------ 256-bit loads ----
+// sm_100 LDG.E.256: one 32-byte sector per thread per instruction.  The BVH
+// nodes (four 32-byte planes/children groups) and the 96-byte triangle
+// records are laid out so every load is one full sector; 16-byte loads of
+// the same data fetch each sector twice (half-used), which was the largest
+// share of the big-scene kernel's L1 wavefronts (ncu, r02a).
+struct __align__(32) F8 {
+    float a, b, c, d, e, f, g, h;
+};
+struct __align__(32) D4 {
+    double x, y, z, w;
+};
+__device__ __forceinline__ F8 ldg_f8(const void* p) {
+    F8 r;
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.a), "=f"(r.b), "=f"(r.c), "=f"(r.d), "=f"(r.e), "=f"(r.f), "=f"(r.g), "=f"(r.h)
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ D4 ldg_d4(const void* p) {
+    D4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+
 // ----------------------------------------------------------- traversal ----
 struct RayF {
     float ox, oy, oz;    // origin * inv (for the FMA slab form)
@@ -318,11 +343,11 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
     n_tris += cnt;
 #endif
     for (uint32_t i = 0; i < cnt; ++i) {
-        const double2* q = reinterpret_cast<const double2*>(tris + start + i);
-        const double2 q0 = __ldg(q + 0), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3),
-                      q4 = __ldg(q + 4);
-        const double v[9] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y, q4.x};
-        const int32_t id = (int32_t)__double_as_longlong(q4.y);
+        const GpuTri* q = tris + start + i;   // 96 bytes: three 256-bit loads
+        const D4 a = ldg_d4(q->v), b = ldg_d4(q->v + 4);
+        const double2 c = __ldg(reinterpret_cast<const double2*>(q->v + 8));
+        const double v[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x};
+        const int32_t id = (int32_t)__double_as_longlong(c.y);
         double t;
         if (mt_hit(ox, oy, oz, dx, dy, dz, v, t_min, h.t, t) && (t < h.t || id < h.id)) {
             h.t = t;
@@ -440,11 +465,12 @@ __device__ __forceinline__ void init_stack(TravStackMem& st, uint2*, uint2* s_st
 // the tree and of the traversal order.  While-while form
 // (Aila & Laine 2009): each lane descends through inner nodes (nearest child
 // first, packed-key sorting network, farther hits pushed) until it holds a
-// leaf, so the expensive f64 leaf tests of a warp run together.  MINMAX
-// selects the forms measured faster in the 512-thread kernel (slab_key_minmax,
-// the register-resident TravStack) over those of the register-starved
-// 768-thread one (slab_key, TravStackMem).
-template <bool MINMAX = true, bool SSTACK = false>
+// leaf, so the expensive f64 leaf tests of a warp run together.  REGSTACK
+// keeps the stack pointer and the shared column address in registers
+// (TravStack); otherwise the stack object lives in local memory
+// (TravStackMem: fewer registers, but every push/pop is local-memory traffic
+// -- 20% of the C5 kernel's L1 wavefronts in r02a, written through to L2).
+template <bool REGSTACK = true, bool SSTACK = false>
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
@@ -457,7 +483,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
     uint2 overflow[SSTACK ? 1 : kStackSize];   // TravStack's local overflow
     typename std::conditional<SSTACK, TravStackShared,
-                              typename std::conditional<MINMAX, TravStack, TravStackMem>::type>::type st;
+                              typename std::conditional<REGSTACK, TravStack, TravStackMem>::type>::type st;
     init_stack(st, overflow, s_stack, s_depth);
     int32_t node = 0;
     bool done = false;
@@ -467,27 +493,14 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
 #ifndef EF_NO_WORK_COUNTERS
             ++n_nodes;
 #endif
-            const float4* q = reinterpret_cast<const float4*>(nodes + node);
-            uint32_t k0, k1, k2, k3;
-            int4 ch;
-            if (MINMAX) {
-                const float4 lx = __ldg(q + 0), hx = __ldg(q + 1), ly = __ldg(q + 2),
-                             hy = __ldg(q + 3), lz = __ldg(q + 4), hz = __ldg(q + 5);
-                ch = __ldg(reinterpret_cast<const int4*>(q + 6));
-                k0 = slab_key_minmax(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tminf, tb, 0u);
-                k1 = slab_key_minmax(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tminf, tb, 1u);
-                k2 = slab_key_minmax(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tminf, tb, 2u);
-                k3 = slab_key_minmax(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tminf, tb, 3u);
-            } else {
-                const float4 nx = __ldg(q + r.nx), fx = __ldg(q + (r.nx ^ 1));
-                const float4 ny = __ldg(q + r.ny), fy = __ldg(q + (r.ny ^ 1));
-                const float4 nz = __ldg(q + r.nz), fz = __ldg(q + (r.nz ^ 1));
-                ch = __ldg(reinterpret_cast<const int4*>(q + 6));
-                k0 = slab_key(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tminf, tb, 0u);
-                k1 = slab_key(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tminf, tb, 1u);
-                k2 = slab_key(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tminf, tb, 2u);
-                k3 = slab_key(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tminf, tb, 3u);
-            }
+            // three 256-bit loads (lo/hi planes of x, y, z), one 128-bit (children)
+            const GpuNode* q = nodes + node;
+            const F8 X = ldg_f8(q->lox), Y = ldg_f8(q->loy), Z = ldg_f8(q->loz);
+            const int4 ch = __ldg(reinterpret_cast<const int4*>(q->child));
+            uint32_t k0 = slab_key_minmax(r, X.a, X.e, Y.a, Y.e, Z.a, Z.e, tminf, tb, 0u);
+            uint32_t k1 = slab_key_minmax(r, X.b, X.f, Y.b, Y.f, Z.b, Z.f, tminf, tb, 1u);
+            uint32_t k2 = slab_key_minmax(r, X.c, X.g, Y.c, Y.g, Z.c, Z.g, tminf, tb, 2u);
+            uint32_t k3 = slab_key_minmax(r, X.d, X.h, Y.d, Y.h, Z.d, Z.h, tminf, tb, 3u);
             kswap(k0, k1);
             kswap(k2, k3);
             kswap(k0, k2);

@@ -21,14 +21,14 @@ constexpr int kTailMaxTris = 4096;   // scenes small enough for the CTA-wide tai
 #endif
 constexpr int kTailCluster = EF_TAIL_CLUSTER;   // leaf-order triangles per tail-sweep cluster
 
-// Four-child BVH node, 128 bytes = eight 16-byte vectors, child boxes in
-// structure-of-arrays form so one node visit is 7 vector loads and four
-// independent slab tests:
+// Four-child BVH node, 128 bytes = four 32-byte sectors, child boxes in
+// structure-of-arrays form so one node visit is three 256-bit loads (x, y, z
+// planes), one 128-bit load (children) and four independent slab tests:
 //   lox, hix, loy, hiy, loz, hiz : float[4]  (conservative f32 child boxes)
 //   child : int32[4]  >= 0 inner node index,
 //                     <  0 leaf ~((start << 3) | (count - 1)),
 //                     kEmptyChild = unused slot
-struct alignas(16) GpuNode {
+struct alignas(32) GpuNode {
     float lox[4], hix[4], loy[4], hiy[4], loz[4], hiz[4];
     int32_t child[4];
     int32_t pad[4];
@@ -36,13 +36,16 @@ struct alignas(16) GpuNode {
 static_assert(sizeof(GpuNode) == 128, "node must be 128 bytes");
 constexpr int32_t kEmptyChild = INT32_MIN;
 
-// f64 triangle payload in BVH leaf order, 80 bytes = 5 x double2:
-// v0.xyz e1.xyz e2.xyz and the original triangle id (as int64 bits).
-struct alignas(16) GpuTri {
+// f64 triangle payload in BVH leaf order, 96 bytes = three 32-byte sectors
+// read by three 256-bit loads (LDG.E.256: one sector each, no half-used
+// sectors as with 16-byte loads of an 80-byte record):
+// v0.xyz e1.xyz e2.xyz, the original triangle id (as int64 bits), padding.
+struct alignas(32) GpuTri {
     double v[9];
     int64_t id;
+    int64_t pad[2];
 };
-static_assert(sizeof(GpuTri) == 80, "tri must be 80 bytes");
+static_assert(sizeof(GpuTri) == 96, "tri must be 96 bytes");
 
 // Per-triangle shading record by original id, 48 bytes: the normal, the
 // diffuse probability p_m of its material and the material index -- one

@@ -41,6 +41,14 @@ static int smem_stack_depth_host() {
 // (A shared-memory copy of the top of the tree measured slower than leaving
 // the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
 // removed; profiles/r01_node_cache_sweep.txt.)
+// Stack form per kernel shape: the register-resident TravStack everywhere
+// unless EF_BIG_STACK_MEM=1 (A/B builds) puts the 768-thread kernel's stack
+// object in local memory as in round 1.
+#ifndef EF_BIG_STACK_MEM
+#define EF_BIG_STACK_MEM 0
+#endif
+template <int THREADS>
+constexpr bool kRegStack = THREADS <= 512 || !EF_BIG_STACK_MEM;
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr size_t kMaxSstackBytes = 128 * 1024;   // leave >= 128 KB of the SM's 256 KB to L1
 constexpr int kMaxSourcesPerLaunch = 256;
@@ -320,7 +328,7 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
             h = closest_brute(s_tri, P.n_tri, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps, INFINITY);
         ls.c[EF_ST_TRIS] += P.n_tri;
     } else {
-        h = closest_bvh<(THREADS <= 512), SSTACK>(P.nodes, P.tris, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz,
+        h = closest_bvh<kRegStack<THREADS>, SSTACK>(P.nodes, P.tris, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz,
                                                   kRayEps, INFINITY, ls.c[EF_ST_NODES],
                                                   ls.c[EF_ST_TRIS], s_stack + threadIdx.x,
                                                   P.smem_stack);
@@ -417,7 +425,7 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
                     else
                         sh = closest_brute(s_tri, P.n_tri, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit);
                 } else {
-                    sh = closest_bvh<(THREADS <= 512), SSTACK>(
+                    sh = closest_bvh<kRegStack<THREADS>, SSTACK>(
                         P.nodes, P.tris, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit,
                         ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], s_stack ? s_stack + threadIdx.x : nullptr,
                         P.smem_stack, true);

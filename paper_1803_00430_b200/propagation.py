@@ -388,13 +388,16 @@ def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceC
     ir = tr.irs()[0]
     paths = tr.path_list() if cfg.er_max_order > 0 else PathList()
     if caches is not None and dt is not None:
-        ir = accumulate_ir(caches.ir.get(key), ir, caches.tau_lr, dt)
-        caches.ir[key] = ir
+        # advance the clock and expire first, so an entry older than 2 tau is
+        # dropped rather than blended into this frame's IR; then blend, store
+        # and mark the entry fresh (the returned IR is the cached one)
         if cfg.er_max_order > 0:
-            paths = caches.update_er(paths, dt)      # advances the cache clock
+            paths = caches.update_er(paths, dt)      # advances the clock, expires ER and IR
         else:
             caches.clock += dt
             caches.expire()
+        ir = accumulate_ir(caches.ir.get(key), ir, caches.tau_lr, dt)
+        caches.ir[key] = ir
         caches.touch_ir(key)
     return paths, ir, tr.trace_stats()[0]
 

@@ -76,15 +76,16 @@ def test_device_tree_small_and_degenerate_counts(n):
 
 
 def test_bounce_loop_on_device_tree_matches_host_tree():
-    """C2 frame slice through ef_trace: identical paths on both trees; the
-    histograms agree to float-atomic ordering."""
+    """C2 frame slice (diffuse rain on, so the histograms carry energy)
+    through ef_trace: identical paths on both trees; the histograms agree to
+    float-atomic ordering."""
     w = workloads.c2_city()
     out = {}
     for build in ("host", "device"):
         sc = _scene(w.tris, w.material_index, w.absorption, w.scattering, build)
         cfg = propagation.TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
                                       bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius,
-                                      seed=w.seed)
+                                      seed=w.seed, diffuse_rain=True)
         tr = propagation.FrameTracer(sc, len(w.sources), cfg, record=True)
         tr.set_sources(w.sources)
         tr.trace(w.listener, n_rays=4096)
@@ -94,6 +95,7 @@ def test_bounce_loop_on_device_tree_matches_host_tree():
     assert np.array_equal(out["host"][0], out["device"][0])
     assert np.array_equal(out["host"][1], out["device"][1])
     Hh, Hd = out["host"][2], out["device"][2]
+    assert sum(st.arrivals for st in out["host"][3]) > 0 and np.abs(Hh).sum() > 0 and np.abs(Hd).sum() > 0
     assert np.allclose(Hh, Hd, rtol=1e-5, atol=1e-6 * np.abs(Hh).max())
     assert out["host"][3][0].total_segments == out["device"][3][0].total_segments
 

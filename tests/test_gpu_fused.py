@@ -37,33 +37,62 @@ def _tracer(w, sc, n_src):
 
 
 def _close(a, b):
+    """Equal up to f32 atomic ordering -- and never a zero-vs-zero pass."""
     scale = float(b.abs().max())
+    assert scale > 0 and float(a.abs().max()) > 0, "vacuous comparison: empty block"
     return torch.allclose(a, b, rtol=1e-5, atol=1e-6 * scale)
+
+
+_C3 = {}
+
+
+def _c3():
+    """C3 interior (closed room: ~2 arrivals per 1,000 segments), 8 sources
+    of 1,024 rays per rank: every owner block of every rank gets splats."""
+    if not _C3:
+        w = workloads.c3_interior(n_sources=8, n_rays=4096)
+        _C3["w"], _C3["sc"] = w, scene_from_workload(w)
+    return _C3["w"], _C3["sc"]
 
 
 @pytest.mark.parametrize("ranks", [2, 4])
 def test_fused_emulated_ranks_equal_unsharded(ranks):
-    w = workloads.c2_city()
-    sc = scene_from_workload(w)
-    S, R = len(w.sources), 2048
+    """Each rank traces rays [r*R, (r+1)*R) of every source with
+    ef_trace_fused into the owners' blocks; every owner block (non-zero)
+    equals the unsharded frame of its sources, and equals what the unfused
+    exchange (per-rank ef_trace partials + a reduce-scatter, summed here as
+    NCCL would) delivers to that owner."""
+    w, sc = _c3()
+    S, R = len(w.sources), 1024
     full = _tracer(w, sc, S)
     part = _tracer(w, sc, S)
     peers = distributed.EmulatedPeers(ranks, S, w.n_bins, sc.n_bands, full.nk)
+    spr = S // ranks
     for frame in (0, 1, 2):
-        full.trace(w.listener, frame=frame, n_rays=ranks * R)
+        full.trace(w.listener, frame=frame, n_rays=ranks * R, total_rays=ranks * R)
         peers.begin_frame(frame)
         segs = 0
+        partial_h, partial_d = [], []
         for r in range(ranks):
             part.trace_fused(w.listener, peers, frame=frame, ray0=r * R, n_rays=R,
                              total_rays=ranks * R)
             segs += int(part.stats[:, 1].sum())
         peers.end_frame()
+        for r in range(ranks):       # the unfused form: local partials of every source
+            part.trace(w.listener, frame=frame, ray0=r * R, n_rays=R, total_rays=ranks * R)
+            partial_h.append(part.H.clone())
+            partial_d.append(part.Dir.clone())
         torch.cuda.synchronize()
-        spr = S // ranks
+        assert int(full.stats[:, 3].min()) > 0          # every source has arrivals
+        rs_h = torch.stack(partial_h).sum(0)             # reduce-scatter: owner r gets rows r*spr..
+        rs_d = torch.stack(partial_d).sum(0)
         for r in range(ranks):
             H, D = peers.block(frame, r)
-            assert _close(H, full.H[r * spr:(r + 1) * spr])
-            assert _close(D, full.Dir[r * spr:(r + 1) * spr])
+            own = slice(r * spr, (r + 1) * spr)
+            assert _close(H, full.H[own]) and _close(D, full.Dir[own])
+            assert _close(H, rs_h[own]) and _close(D, rs_d[own])
+            for j in range(spr):                          # every owned source block is non-zero
+                assert float(H[j].abs().sum()) > 0
         assert segs == int(full.stats[:, 1].sum())
 
 

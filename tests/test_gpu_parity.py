@@ -16,8 +16,7 @@ if not torch.cuda.is_available():
 from oracle import analysis as OA  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_1803_00430_b200 import _lib, analysis, bvh, propagation, scene, sh, workloads  # noqa: E402
-
-HIST_RTOL = 1e-4
+from _gpu_common import hist_close, is_documented_near_tie  # noqa: E402
 
 
 def _scene_from_golden(g):
@@ -80,7 +79,12 @@ def test_soup_bvh_vs_reference(golden):
     s = _scene_from_golden(g)
     t, tri, hit = s.bvh.intersect_batch(g["origins"], g["dirs"], 1e-4)
     mism = np.nonzero(tri != g["bvh_tri"])[0]
-    assert len(mism) <= 2
+    # every differing id must be a documented near-tie: a
+    # hit within 1e-6 of an edge, where the reference's BLAS-ordered v can
+    # flip, or an exact t tie (the reference BVH keeps the last visited)
+    for i in mism:
+        assert is_documented_near_tie(g["origins"][i], g["dirs"][i], int(tri[i]), int(g["bvh_tri"][i]),
+                                      g["v0"], g["e1"], g["e2"]), i
     same = tri == g["bvh_tri"]
     assert np.array_equal(t[same & hit], g["bvh_t"][same & hit])
     # brute force (intersect_brute, scene.py:194) is exact
@@ -89,7 +93,9 @@ def test_soup_bvh_vs_reference(golden):
     assert np.array_equal(tb[hitb], g["brute_t"][hitb])
     # intersect_batch takes the BVH path for 700 > 512 triangles
     t2, tri2, _ = s.intersect_batch(g["origins"][:2000], g["dirs"][:2000])
-    assert (tri2 != g["batch_tri"]).sum() <= 1
+    for i in np.nonzero(tri2 != g["batch_tri"])[0]:
+        assert is_documented_near_tie(g["origins"][i], g["dirs"][i], int(tri2[i]), int(g["batch_tri"][i]),
+                                      g["v0"], g["e1"], g["e2"]), i
 
 
 def test_city_bvh_queries(golden):
@@ -113,8 +119,14 @@ def test_occluded_batch_matches_oracle(golden):
     delta = tg - o
     dist = np.linalg.norm(delta, axis=1)
     d = delta / np.maximum(dist, 1e-12)[:, None]
-    _, tri, _ = os_.intersect_batch(o, d, t_max=dist - 1e-4, mode=2)
-    assert (occ != (tri >= 0)).sum() <= 1
+    t_o, tri, _ = os_.intersect_batch(o, d, t_max=dist - 1e-4, mode=2)
+    # a differing answer must be a documented near-tie: the blocker's hit
+    # within 1e-6 of an edge, or its t within 1e-12 of the limit (the two
+    # sides' t <= limit / t < limit conventions, scene.py:247-250)
+    for i in np.nonzero(occ != (tri >= 0))[0]:
+        _, tri_c, _ = os_.intersect_batch(o[i:i + 1], d[i:i + 1], mode=1)   # closest, no limit
+        assert is_documented_near_tie(o[i], d[i], int(tri[i]), int(tri_c[0]), g["v0"], g["e1"], g["e2"],
+                                      t_limit=dist[i] - 1e-4), i
     assert occ.any() and (~occ).any()
 
 
@@ -176,18 +188,7 @@ def _oracle_trace(os_, w, src_index, rays, record=True, frame=0):
 
 
 def _hist_close(Hg, Ho):
-    """1e-4 relative per bin on bins with > 1e-6 of the band's energy."""
-    Hg = np.asarray(Hg, np.float64)
-    for b in range(Ho.shape[1]):
-        tot = np.abs(Ho[:, b, 0]).sum()
-        if tot == 0:
-            assert np.abs(Hg[:, b, :]).max() == 0
-            continue
-        sig = np.abs(Ho[:, b, 0]) > 1e-6 * tot
-        for k in range(Ho.shape[2]):
-            a, r = Hg[sig, b, k], Ho[sig, b, k]
-            scale = np.maximum(np.abs(r), np.abs(Ho[sig, b, 0]))
-            assert np.all(np.abs(a - r) <= HIST_RTOL * scale), (b, k)
+    hist_close(Hg, Ho)   # 1e-4 per significant bin; both sides must carry energy
 
 
 def test_c1_full_parity():
@@ -284,10 +285,12 @@ def test_c2_tail_kernel_paths_exact():
         ref = _oracle_trace(os_, w, 6, rays)
         bad, excl = _compare_paths(tr.path_nseg.cpu().numpy()[0], tr.path_ids.cpu().numpy()[0], ref)
         assert bad == 0 and excl <= 3
+        st = tr.stats.cpu().numpy()[0]
         if len(rays) == 1:
-            st = tr.stats.cpu().numpy()[0]
             assert tr.path_nseg.cpu().numpy()[0, 0] == 100 == st[1]
-            assert st[7] < st[1]   # ~no node visits: every segment came from the tail sweep
+            assert st[9] == st[1]   # EF_ST_TAIL: every segment ran in the tail kernel
+        else:
+            assert st[9] > 0
 
 
 def test_c2_matches_reference_driven_golden(golden):
@@ -310,7 +313,6 @@ def test_c2_full_frame_properties():
         assert st[s].total_segments == int(nseg[s].sum())
         assert st[s].reflections == st[s].total_segments - st[s].escaped
         assert nseg[s].min() >= 1 and nseg[s].max() <= w.max_bounces
-    H_full = tr.H.clone()
     half = w.n_rays // 2
     tr.record = False
     tr.trace(w.listener, n_rays=half, total_rays=w.n_rays)
@@ -320,24 +322,8 @@ def test_c2_full_frame_properties():
     for s in range(len(w.sources)):
         assert st2[s].total_segments == st[s].total_segments
         assert st2[s].arrivals == st[s].arrivals
-    Hf = H_full.cpu().numpy().astype(np.float64)
-    Hs = tr.H.cpu().numpy().astype(np.float64)
-    for s in range(len(w.sources)):
-        _hist_close(Hs[s], Hf[s])
-    # energy bound: per-band arrival energy <= e0 * rays * max segments
-    assert np.all(Hf[..., 0] >= 0)
-
-
-def test_c2_histogram_subsample_vs_oracle():
-    w = workloads.c2_city()
-    n = 4096
-    _, _, tr = _run_gpu(w, n_rays=n, record=False, sources=[0, 1])
-    os_ = _oracle_for(w)
-    for j, s in enumerate([0, 1]):
-        ref = _oracle_trace(os_, w, s, np.arange(n, dtype=np.uint32), record=True)
-        if (ref.first_tie >= 0).any():
-            pytest.skip("near-tie path in subsample")
-        _hist_close(tr.H[j].cpu().numpy(), ref.H)
+    # (the open city frame has no arrivals at this ray count: histogram shard
+    # invariance is tested with diffuse rain, test_gpu_histograms.py)
 
 
 # -------------------------------------------------------------- estimators
@@ -413,7 +399,10 @@ def test_large_scene_subsample_parity(name, n, srcs):
         bad, e = _compare_paths(nseg[j], ids[j], ref)
         assert bad == 0, (name, s, bad)
         excl += e
-        if e == 0:
+        assert tr.trace_stats()[j].arrivals == ref.stats["arrivals"] or e > 0
+        if name == "c3":
+            assert ref.stats["arrivals"] > 0
+        if e == 0 and ref.stats["arrivals"] > 0:   # C5 arrivals: test_gpu_histograms.py
             _hist_close(tr.H[j].cpu().numpy(), ref.H)
     assert excl <= 0.02 * n * len(srcs)
 
