@@ -357,27 +357,30 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
     }
 }
 
-// Traversal stack: entries [0, depth) live in shared memory (i-major, one
-// column per thread: conflict-free and immune to L1 thrashing by node and
-// triangle traffic), deeper entries in local memory.  Entry = (node, key).
-// The scalars stay in registers and the shared column is addressed through
-// a 32-bit shared-window address (st.shared / ld.shared), so a push is one
-// STS instead of a generic store plus local-memory bookkeeping.
-constexpr int kSmemStack = 16;   // max shared entries per thread (runtime depth <= this)
+// Traversal stacks.  Entry = (node, key).  The trace kernels keep a thread's
+// stack top in a shared-memory column (i-major: entry i of thread t at
+// base + i * STEP + 8 t, conflict-free and immune to L1 thrashing by node and
+// triangle traffic), addressed by a 32-bit shared-window address in a
+// register; DEPTH and STEP are compile-time constants, so a push is one STS
+// at sbase + sp * STEP.  (A runtime depth / stride with a null-column check
+// made the compiler rebuild the column address from the shared window base
+// on every push and pop: ~13% of the C5 kernel's instructions, r02c.)
+constexpr int kSmemStack = 16;   // max shared entries per thread
 
-struct TravStack {
+// Shared top (DEPTH entries) + local-memory overflow (rarely touched).
+template <int DEPTH, uint32_t STEP>
+struct StackSplit {
+    static constexpr bool kPredicated = false;
     uint32_t sbase;  // shared address of this thread's column
-    uint32_t sstep;  // bytes between consecutive entries of a column (8 * blockDim.x)
-    int depth;       // shared entries per thread
     int sp;
-    uint2* l;        // local-memory overflow array (kept outside this struct so
-                     // the scalars above can live in registers)
+    uint2* l;        // local-memory overflow array (outside the struct, so the
+                     // scalars can live in registers)
 
     __device__ __forceinline__ void push(int32_t node, uint32_t key) {
-        if (sp < depth) {
+        if (sp < DEPTH) {
             // volatile asm keeps push/pop order; no memory clobber, so global
             // loads (nodes, triangles) still schedule freely around it
-            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sbase + (uint32_t)sp * sstep),
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sbase + (uint32_t)sp * STEP),
                          "r"((uint32_t)node), "r"(key));
         } else {
             l[sp] = make_uint2((uint32_t)node, key);
@@ -385,79 +388,54 @@ struct TravStack {
         ++sp;
     }
     __device__ __forceinline__ uint2 top() const {
-        if (sp < depth) {
+        if (sp < DEPTH) {
             uint2 e;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
-                         : "r"(sbase + (uint32_t)sp * sstep));
+                         : "r"(sbase + (uint32_t)sp * STEP));
             return e;
         }
         return l[sp];
     }
 };
 
-// The same stack with its scalars and overflow array in one local-memory
-// object and a generic pointer to the shared column.  Measured faster in the
-// register-starved 768-thread kernel on C3 (62.6 vs 72.5 ms per frame, the
-// register-resident form frees fewer registers than it costs there), slower
-// in the 512-thread one (C2 0.665 vs 0.649 ms).
-struct TravStackMem {
-    uint2* s;        // shared column base (nullptr: local only)
-    int stride;      // blockDim.x
-    int depth;       // shared entries per thread
-    uint2 l[kStackSize];
-    int sp;
-
-    __device__ __forceinline__ void push(int32_t node, uint32_t key) {
-        const uint2 e = make_uint2((uint32_t)node, key);
-        if (sp < depth) s[sp * stride] = e;
-        else l[sp] = e;
-        ++sp;
-    }
-    __device__ __forceinline__ uint2 top() const { return sp < depth ? s[sp * stride] : l[sp]; }
-};
-
-// The whole stack in shared memory (the host guarantees depth >= the tree's
-// max_stack): pushes are predicated stores, no overflow branch.
-struct TravStackShared {
+// The whole stack in shared memory (the host guarantees the column holds the
+// tree's max_stack): pushes are predicated stores, no overflow branch.
+template <uint32_t STEP>
+struct StackShared {
+    static constexpr bool kPredicated = true;
     uint32_t sbase;
-    uint32_t sstep;
     int sp;
 
     // push `node, key` if `valid` (no branch: predicated st.shared)
     __device__ __forceinline__ void push_if(int32_t node, uint32_t key, bool valid) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-            "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(sbase + (uint32_t)sp * sstep),
+            "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(sbase + (uint32_t)sp * STEP),
             "r"((uint32_t)node), "r"(key), "r"((uint32_t)valid));
         sp += valid ? 1 : 0;
     }
     __device__ __forceinline__ uint2 top() const {
         uint2 e;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
-                     : "r"(sbase + (uint32_t)sp * sstep));
+                     : "r"(sbase + (uint32_t)sp * STEP));
         return e;
     }
 };
 
-__device__ __forceinline__ void init_stack(TravStackShared& st, uint2*, uint2* s_stack, int) {
-    st.sbase = (uint32_t)__cvta_generic_to_shared(s_stack);
-    st.sstep = 8u * blockDim.x;
-    st.sp = 0;
-}
+// Local memory only (the query kernels: no shared memory).
+struct StackLocal {
+    static constexpr bool kPredicated = false;
+    uint2 l[kStackSize];
+    int sp;
+    __device__ __forceinline__ void push(int32_t node, uint32_t key) {
+        l[sp++] = make_uint2((uint32_t)node, key);
+    }
+    __device__ __forceinline__ uint2 top() const { return l[sp]; }
+};
 
-__device__ __forceinline__ void init_stack(TravStack& st, uint2* overflow, uint2* s_stack,
-                                           int s_depth) {
-    st.l = overflow;
-    st.sbase = s_stack ? (uint32_t)__cvta_generic_to_shared(s_stack) : 0u;
-    st.sstep = 8u * blockDim.x;
-    st.depth = s_stack ? s_depth : 0;
-    st.sp = 0;
-}
-__device__ __forceinline__ void init_stack(TravStackMem& st, uint2*, uint2* s_stack, int s_depth) {
-    st.s = s_stack;
-    st.stride = blockDim.x;
-    st.depth = s_stack ? s_depth : 0;
-    st.sp = 0;
+// shared-window address of this thread's column of the stack area s_stack
+__device__ __forceinline__ uint32_t stack_column(const uint2* s_stack) {
+    return (uint32_t)__cvta_generic_to_shared(s_stack) + 8u * threadIdx.x;
 }
 
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
@@ -465,26 +443,18 @@ __device__ __forceinline__ void init_stack(TravStackMem& st, uint2*, uint2* s_st
 // the tree and of the traversal order.  While-while form
 // (Aila & Laine 2009): each lane descends through inner nodes (nearest child
 // first, packed-key sorting network, farther hits pushed) until it holds a
-// leaf, so the expensive f64 leaf tests of a warp run together.  REGSTACK
-// keeps the stack pointer and the shared column address in registers
-// (TravStack); otherwise the stack object lives in local memory
-// (TravStackMem: fewer registers, but every push/pop is local-memory traffic
-// -- 20% of the C5 kernel's L1 wavefronts in r02a, written through to L2).
-template <bool REGSTACK = true, bool SSTACK = false>
+// leaf, so the expensive f64 leaf tests of a warp run together.  The stack
+// (st, empty on entry) is one of the forms above.
+template <typename StackT>
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max, uint32_t& n_nodes, uint32_t& n_tris,
-                                           uint2* s_stack = nullptr, int s_depth = 0,
-                                           bool any_hit = false) {
+                                           StackT& st, bool any_hit = false) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
-    uint2 overflow[SSTACK ? 1 : kStackSize];   // TravStack's local overflow
-    typename std::conditional<SSTACK, TravStackShared,
-                              typename std::conditional<REGSTACK, TravStack, TravStackMem>::type>::type st;
-    init_stack(st, overflow, s_stack, s_depth);
     int32_t node = 0;
     bool done = false;
     for (;;) {
@@ -506,7 +476,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
-            if constexpr (SSTACK) {
+            if constexpr (StackT::kPredicated) {
                 st.push_if(pick(ch, k3 & 3u), k3, k3 != 0xffffffffu);
                 st.push_if(pick(ch, k2 & 3u), k2, k2 != 0xffffffffu);
                 st.push_if(pick(ch, k1 & 3u), k1, k1 != 0xffffffffu);
@@ -556,12 +526,33 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
     }
 }
 
+// The trace kernels' forms: the whole stack in shared memory (SSTACK), or
+// its top DEPTH entries there and the rest in local memory; THREADS columns.
+template <int THREADS, int DEPTH, bool SSTACK>
+__device__ __forceinline__ Hit closest_bvh_column(const GpuNode* __restrict__ nodes,
+                                                  const GpuTri* __restrict__ tris, double ox,
+                                                  double oy, double oz, double dx, double dy,
+                                                  double dz, double t_min, double t_max,
+                                                  uint32_t& n_nodes, uint32_t& n_tris,
+                                                  const uint2* s_stack, bool any_hit = false) {
+    if constexpr (SSTACK) {
+        StackShared<8u * THREADS> st{stack_column(s_stack), 0};
+        return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
+    } else {
+        uint2 overflow[kStackSize];
+        StackSplit<DEPTH, 8u * THREADS> st{stack_column(s_stack), 0, overflow};
+        return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
+    }
+}
+
 __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max) {
     uint32_t a = 0, b = 0;
-    return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, a, b);
+    StackLocal st;
+    st.sp = 0;
+    return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, a, b, st);
 }
 
 // ------------------------------------------------------------------ SH ----

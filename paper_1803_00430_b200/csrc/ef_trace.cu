@@ -25,30 +25,14 @@ namespace ef {
 constexpr int kSmallThreads = 512;
 constexpr int kBigThreads = 768;
 constexpr int64_t kBigSceneBytes = 4ll << 20;
+// Shared traversal-stack entries per thread (the rest in local memory) when
+// the tree's whole stack does not fit: 16 x 512 threads (64 KB) or
+// 12 x 768 (72 KB), columns for THREADS threads (compile-time stride).
 template <int THREADS>
-constexpr int smem_stack_depth_default() { return THREADS <= 512 ? 16 : 12; }
-// EF_SMEM_STACK overrides the shared stack entries per thread (tuning; the
-// rest of the stack lives in local memory)
-template <int THREADS>
-static int smem_stack_depth_host() {
-    static const int v = [] {
-        const char* e = std::getenv("EF_SMEM_STACK");
-        const int d = e ? std::atoi(e) : smem_stack_depth_default<THREADS>();
-        return std::max(0, std::min(d, kSmemStack));
-    }();
-    return v;
-}
+constexpr int kSplitDepth = THREADS <= 512 ? 16 : 12;
 // (A shared-memory copy of the top of the tree measured slower than leaving
 // the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
 // removed; profiles/r01_node_cache_sweep.txt.)
-// Stack form per kernel shape: the register-resident TravStack everywhere
-// unless EF_BIG_STACK_MEM=1 (A/B builds) puts the 768-thread kernel's stack
-// object in local memory as in round 1.
-#ifndef EF_BIG_STACK_MEM
-#define EF_BIG_STACK_MEM 0
-#endif
-template <int THREADS>
-constexpr bool kRegStack = THREADS <= 512 || !EF_BIG_STACK_MEM;
 constexpr size_t kMaxTraceSmem = 220 * 1024;
 constexpr size_t kMaxSstackBytes = 128 * 1024;   // leave >= 128 KB of the SM's 256 KB to L1
 constexpr int kMaxSourcesPerLaunch = 256;
@@ -149,6 +133,7 @@ struct TraceParams {
     float* Dp[kMaxRanks];
     int32_t spr;
     int32_t src0;           // global index of this launch's source 0
+    int32_t vec_red;        // blocks are local: commit with 16-byte vector reductions
     unsigned long long* stats;
     double* sum_t;
     int32_t* path_nseg;
@@ -208,6 +193,62 @@ __device__ __forceinline__ float* peer_block(float* const (&tab)[kMaxRanks], con
     return tab[o] + (size_t)(g - o * P.spr) * per;
 }
 
+// Adds one arrival's splat c[b] * Y[k] (b < nb, k < NK) into the nb * NK
+// contiguous floats at dst.  Warp-aggregated: the lanes committing together
+// are grouped by destination (__match_any_sync on the block address -- the
+// same source's Dir block, or the same histogram bin); a group's leader
+// alone commits the group's sum (shuffled from its peers, in lane order).
+// With local blocks the commit is 16-byte vector reductions
+// (red.global.add.v4.f32; nb * NK is a multiple of 4 for nb in {4, 8}, and
+// every bin / block starts on a 16-byte boundary): nb * NK / 4 requests per
+// arrival instead of nb * NK.
+template <int NBMAX, int NK>
+__device__ __forceinline__ void commit_splat(const TraceParams& P, float* dst, const float* c,
+                                             const float* Yf) {
+    const int nb = P.nb;
+    const unsigned am = __activemask();
+    const unsigned peers = __match_any_sync(am, reinterpret_cast<unsigned long long>(dst));
+    const int lane = threadIdx.x & 31;
+    const bool lead = lane == __ffs(peers) - 1;
+    if (P.vec_red && (nb * NK) % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < NBMAX * NK; j += 4) {
+            if (j < nb * NK) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = c[(j + q) / NK] * Yf[(j + q) % NK];
+                if (peers != (1u << lane)) {   // rare: several lanes, one destination
+                    float a[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (unsigned rest = peers; rest; rest &= rest - 1) {
+                        const int p = __ffs(rest) - 1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) a[q] += __shfl_sync(peers, v[q], p);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[q] = a[q];
+                }
+                if (lead)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + j),
+                                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+                                 : "memory");
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NBMAX * NK; ++j) {
+            if (j < nb * NK) {
+                float v = c[j / NK] * Yf[j % NK];
+                if (peers != (1u << lane)) {
+                    float a = 0.f;
+                    for (unsigned rest = peers; rest; rest &= rest - 1) a += __shfl_sync(peers, v, __ffs(rest) - 1);
+                    v = a;
+                }
+                if (lead) atomicAdd(dst + j, v);
+            }
+        }
+    }
+}
+
 // One listener arrival of order `order` (reflections before it) at path
 // length `dist` from arrival direction (ux,uy,uz) with per-band energies c[]:
 // order 0 -> Dir, 1..er_max_order -> early-reflection list (when enabled),
@@ -252,13 +293,7 @@ __device__ __forceinline__ void commit_arrival(const TraceParams& P, int src, in
         float Yf[NK];
 #pragma unroll
         for (int k = 0; k < NK; ++k) Yf[k] = (float)Y[k];
-#pragma unroll
-        for (int b = 0; b < NBMAX; ++b) {
-            if (b < nb) {
-#pragma unroll
-                for (int k = 0; k < NK; ++k) atomicAdd(dst + b * NK + k, c[b] * Yf[k]);
-            }
-        }
+        commit_splat<NBMAX, NK>(P, dst, c, Yf);
     }
 }
 
@@ -328,10 +363,9 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
             h = closest_brute(s_tri, P.n_tri, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps, INFINITY);
         ls.c[EF_ST_TRIS] += P.n_tri;
     } else {
-        h = closest_bvh<kRegStack<THREADS>, SSTACK>(P.nodes, P.tris, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz,
-                                                  kRayEps, INFINITY, ls.c[EF_ST_NODES],
-                                                  ls.c[EF_ST_TRIS], s_stack + threadIdx.x,
-                                                  P.smem_stack);
+        h = closest_bvh_column<THREADS, kSplitDepth<THREADS>, SSTACK>(
+            P.nodes, P.tris, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps, INFINITY, ls.c[EF_ST_NODES],
+            ls.c[EF_ST_TRIS], s_stack);
     }
     finish_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, h, s_tri, s_stack, lg);
 }
@@ -425,10 +459,16 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
                     else
                         sh = closest_brute(s_tri, P.n_tri, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit);
                 } else {
-                    sh = closest_bvh<kRegStack<THREADS>, SSTACK>(
-                        P.nodes, P.tris, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit,
-                        ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], s_stack ? s_stack + threadIdx.x : nullptr,
-                        P.smem_stack, true);
+                    if constexpr (G == 1)   // trace kernels: this thread's stack column
+                        sh = closest_bvh_column<THREADS, kSplitDepth<THREADS>, SSTACK>(
+                            P.nodes, P.tris, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit,
+                            ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], s_stack, true);
+                    else {                  // tail kernel (a whole CTA per path): local stack
+                        StackLocal ls_st;
+                        ls_st.sp = 0;
+                        sh = closest_bvh(P.nodes, P.tris, S.ox, S.oy, S.oz, ex, ey, ez, kRayEps, limit,
+                                         ls.c[EF_ST_NODES], ls.c[EF_ST_TRIS], ls_st, true);
+                    }
                 }
                 if (sh.id == INT32_MAX && lead) {
                     const float gf = (float)(cosv * P.r2 / d2);
@@ -522,15 +562,19 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
     static_assert(G == 1 || BRUTE, "lane groups are for the all-pairs path");
     pdl_trigger();   // the tail / analysis kernel may be scheduled onto SMs this grid frees
     extern __shared__ __align__(16) unsigned char smem[];
-    // per-block counters: f64 path-length sums, then u32 counters (a block's
-    // per-source counts stay far below 2^32), then the all-pairs triangles
-    double* s_sumt = reinterpret_cast<double*>(smem);
+    // traversal stacks first (P.smem_stack entries per thread, i-major), so a
+    // thread's column address is the shared symbol + 8 * threadIdx.x -- cheap
+    // to keep or rematerialise (derived through a 64-bit generic pointer it
+    // was rebuilt from the shared window base on every pop: ~13% of the C5
+    // kernel's instructions, r02c source counters); then the per-block
+    // counters (f64 path-length sums, u32 counters: a block's per-source
+    // counts stay far below 2^32) and the all-pairs triangles
+    uint2* s_stack = reinterpret_cast<uint2*>(smem);
+    const uint32_t stack_bytes = BRUTE ? 0u : (uint32_t)P.smem_stack * THREADS * 8u;
+    double* s_sumt = reinterpret_cast<double*>(smem + stack_bytes);
     unsigned int* s_stats = reinterpret_cast<unsigned int*>(s_sumt + P.n_src);
     double* s_tri = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(s_stats + P.n_src * EF_ST_COUNT) + 15) & ~uintptr_t(15));
-    // traversal stacks (P.smem_stack entries per thread)
-    uint2* s_stack = reinterpret_cast<uint2*>(
-        (reinterpret_cast<uintptr_t>(s_tri) + 15) & ~uintptr_t(15));
+        smem + ((stack_bytes + 8u * P.n_src + 4u * P.n_src * EF_ST_COUNT + 15u) & ~15u));
     for (int i = threadIdx.x; i < P.n_src * EF_ST_COUNT; i += blockDim.x) s_stats[i] = 0u;
     for (int i = threadIdx.x; i < P.n_src; i += blockDim.x) s_sumt[i] = 0.0;
     if (BRUTE)
@@ -828,7 +872,7 @@ static int sm_count() {
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
 static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     TraceParams P = P0;
-    if (!SSTACK) P.smem_stack = smem_stack_depth_host<THREADS>();   // else: the tree's max_stack
+    if (!SSTACK) P.smem_stack = kSplitDepth<THREADS>;   // else: the tree's max_stack
     // Too few paths to give every SM a full CTA (C1: 4,096 paths): spread them
     // over all SMs in smaller CTAs (>= one warp), so each path's latency-bound
     // chain shares its SM with as few others as possible.
@@ -844,7 +888,7 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
         block = (int)std::min<long long>(THREADS, std::max<long long>(32, (per + 31) / 32 * 32));
     }
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
-                  (BRUTE ? 0 : (size_t)P.smem_stack * block * sizeof(uint2));
+                  (BRUTE ? 0 : (size_t)P.smem_stack * THREADS * sizeof(uint2));   // THREADS columns
     auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
@@ -1250,6 +1294,9 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
             P.spr = ns;
             P.src0 = 0;
         }
+        // vector reductions into this GPU's own blocks; scalar f32 reds over
+        // the peer mapping (remote NVLink targets)
+        P.vec_red = fused ? 0 : 1;
         P.stats = stats + (size_t)s0 * EF_ST_COUNT;
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;

@@ -25,37 +25,49 @@ def hist_close(Hg, Ho, require_signal=True):
             assert np.all(np.abs(a - r) <= HIST_RTOL * scale), (b, k)
 
 
-def arriving_rays(tracer, listener, n_rays_norm, lo, hi, want, chunk=1 << 15):
-    """Global ray indices in [lo, hi) of the tracer's single source whose
-    paths reach the listener (recorded GPU pre-pass: chunks are traced and
-    those with arrivals bisected down to single rays).  The counter-based
-    RNG makes any subset reproducible, so the oracle can trace exactly
-    these rays.  Returns at most ``want`` indices, ascending."""
+def arriving_rays(scene, cfg, sources, keys, listener, n_rays_norm, scan, want, chunk=1 << 16):
+    """(source index, global ray indices) pairs whose paths reach the
+    listener (recorded GPU pre-pass): chunks of rays of ALL sources are
+    traced in one launch each, and the sources with arrivals in a chunk are
+    bisected down to single rays with a one-source tracer.  The
+    counter-based RNG makes any subset reproducible, so the oracle can trace
+    exactly these rays.  Returns {source index: uint32 ray ids}, at most
+    ``want`` rays in total."""
     import torch
 
-    def arrivals(a, n):
-        tracer.trace(listener, ray0=a, n_rays=n, total_rays=n_rays_norm)
-        torch.cuda.synchronize()
-        return int(tracer.stats[0, 3])
+    from paper_1803_00430_b200 import propagation
+    allt = propagation.FrameTracer(scene, len(sources), cfg)
+    allt.set_sources(sources, keys)
+    one = propagation.FrameTracer(scene, 1, cfg)
 
-    found = []
-    for a in range(lo, hi, chunk):
-        n = min(chunk, hi - a)
-        if arrivals(a, n) == 0:
-            continue
-        todo = [(a, n)]
-        while todo:
-            b, m = todo.pop()
-            if m == 1:
-                found.append(b)
-                continue
-            h = m // 2
-            for c, k in ((b, h), (b + h, m - h)):
-                if arrivals(c, k) > 0:
-                    todo.append((c, k))
-        if len(found) >= want:
+    def arrivals_one(a, n):
+        one.trace(listener, ray0=a, n_rays=n, total_rays=n_rays_norm)
+        torch.cuda.synchronize()
+        return int(one.stats[0, 3])
+
+    found = {}
+    total = 0
+    for a in range(0, scan, chunk):
+        n = min(chunk, scan - a)
+        allt.trace(listener, ray0=a, n_rays=n, total_rays=n_rays_norm)
+        torch.cuda.synchronize()
+        per_src = allt.stats[:, 3].cpu().numpy()
+        for s in np.nonzero(per_src > 0)[0]:
+            one.set_sources(np.asarray(sources)[[s]], [int(keys[s])])
+            todo = [(a, n)]
+            while todo:
+                b, m = todo.pop()
+                if m == 1:
+                    found.setdefault(int(s), []).append(b)
+                    total += 1
+                    continue
+                h = m // 2
+                for c, k in ((b, h), (b + h, m - h)):
+                    if arrivals_one(c, k) > 0:
+                        todo.append((c, k))
+        if total >= want:
             break
-    return np.array(sorted(found)[:want], np.uint32)
+    return {s: np.array(sorted(r), np.uint32) for s, r in found.items()}
 
 
 def mt_uvt(o, d, v0, e1, e2):

@@ -1,0 +1,28 @@
+#!/bin/bash
+# Env-knob sweep of bench lines on one box:
+#   SWEEP="EF_DYN=0|EF_DYN=1 EF_DYN_T=16|..." CONFIGS="c5 c3" TAG=x bash tools/gpu_sweep.sh
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/${TAG:-sweep}
+mkdir -p $O
+if [ "${TESTS:-0}" = 1 ]; then
+  timeout 900 python -m pytest tests -m gpu -q -x ${TESTARGS:-} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+  tail -5 $O/pytest_gpu.log
+fi
+IFS='|' read -ra VARIANTS <<< "${SWEEP:-}"
+for rep in $(seq 1 ${REPS:-1}); do
+for v in "${VARIANTS[@]}"; do
+  for c in ${CONFIGS:-c5}; do
+    st=20; [ $c = c5 ] && st=5; [ $c = c2 ] && st=100; [ $c = c1 ] && st=100
+    env $v timeout 900 python bench.py --config $c --steps $st --warmup 3 --no-cpu-baseline > $O/b.jsonl 2> $O/b.err
+    python - "$v" "$c" $O/b.jsonl <<'PY'
+import json, sys
+try:
+    d = json.loads([l for l in open(sys.argv[3]) if l.startswith('{')][-1])
+    r = d.get('roofline_device') or {}
+    print(f"{sys.argv[1]:40s} {sys.argv[2]} {d['value']/1e9:.4f} G/s {d['ms_per_step']:.3f} ms nodes/seg {r.get('nodes_per_segment', 0):.2f} clk {d.get('clocks', {}).get('sm_mhz')}", flush=True)
+except Exception as e:
+    print(sys.argv[1], sys.argv[2], 'failed', e, open(sys.argv[3].replace('.jsonl', '.err')).read()[-600:])
+PY
+  done
+done
+done
