@@ -19,17 +19,24 @@
 
 namespace ef {
 
-// One fat CTA per SM (node cache in shared memory).  Scenes whose nodes +
-// triangles exceed kBigSceneBytes (L1 cannot hold the scene: C3, C5) get
-// 768 threads (80 registers, more warps to hide latency); smaller ones 512.
+// One fat CTA per SM: 512 threads, 128 registers.  (Scenes whose nodes +
+// triangles exceed kBigSceneBytes -- L1 cannot hold them: C3, C5 -- ran 768
+// threads at 80 registers in round 1; with the compile-time stack shapes the
+// 512-thread kernel is faster there too: C5 3.84 vs 3.62 (768) / 3.71 (640)
+// / 3.32 (384) G seg/s, C3 2.39 vs 2.38 / 2.42 / 2.05, r02f.)  Big scenes
+// keep the split stack (shared top + local overflow) since their trees'
+// whole stack does not fit in shared memory.
 constexpr int kSmallThreads = 512;
-constexpr int kBigThreads = 768;
 constexpr int64_t kBigSceneBytes = 4ll << 20;
 // Shared traversal-stack entries per thread (the rest in local memory) when
-// the tree's whole stack does not fit: 16 x 512 threads (64 KB) or
-// 12 x 768 (72 KB), columns for THREADS threads (compile-time stride).
+// the tree's whole stack does not fit: 12 x 512 threads (48 KB), columns for
+// THREADS threads (compile-time stride).  (8 / 12 / 16 entries: C5 3.867 /
+// 3.862 / 3.839, C3 2.384 / 2.398 / 2.389 G seg/s, r02i -- flat.)
+#ifndef EF_SPLIT_DEPTH
+#define EF_SPLIT_DEPTH 12
+#endif
 template <int THREADS>
-constexpr int kSplitDepth = THREADS <= 512 ? 16 : 12;
+constexpr int kSplitDepth = EF_SPLIT_DEPTH;
 // (A shared-memory copy of the top of the tree measured slower than leaving
 // the space to L1 -- C5 2.93 vs 3.34 G seg/s with 128 KB, C2 flat -- and was
 // removed; profiles/r01_node_cache_sweep.txt.)
@@ -983,7 +990,7 @@ static cudaError_t dispatch(bool brute, bool big, int order, const TraceParams& 
             default: return dispatch_order<NBMAX, true, kSmallThreads>(order, P, st);
         }
     }
-    if (big) return dispatch_order<NBMAX, false, kBigThreads>(order, P, st);
+    if (big) return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
     if (P.smem_stack > 0) return dispatch_order<NBMAX, false, kSmallThreads, 1, true>(order, P, st);
     return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
 }
