@@ -207,7 +207,7 @@ def config_block(args, w, world, exchange=None):
             "sh_order": int(w.order), "bands": int(w.n_bands), "bins": int(w.n_bins),
             "parallelism": (f"each source's rays sharded x{world} (fixed frame), " + (
                 "histograms reduce-scattered inside the trace kernel (ef_trace_fused, peer memory)"
-                if exchange == "fused" else "NCCL reduce-scatter of histograms")) if world > 1
+                if exchange == "fused" else "NCCL reduce-scatter of histograms (ef_nccl_reduce_hist)")) if world > 1
             else "single GPU", "l2": "flushed between steps (256 MiB write)"}
 
 
@@ -253,6 +253,10 @@ def run_gpu(args, w, metric, unit):
             fused = False
             exchange_note = f"fused exchange unavailable ({e}); NCCL reduce-scatter used"
     if world > 1 and not fused:
+        # unfused exchange through the C ABI (ef_nccl_reduce_hist) for the
+        # histograms; the small per-source counters through torch's NCCL
+        from paper_1803_00430_b200.distributed import NcclHistExchange
+        nccl_ex = NcclHistExchange(world, rank, local)
         H_own = torch.empty((S_own,) + tuple(tr.H.shape[1:]), dtype=torch.float32, device=dev)
         D_own = torch.empty((S_own,) + tuple(tr.Dir.shape[1:]), dtype=torch.float32, device=dev)
         st_own = torch.empty((S_own, tr.stats.shape[1]), dtype=torch.int64, device=dev)
@@ -310,8 +314,8 @@ def run_gpu(args, w, metric, unit):
             own = slice(rank * S_own, (rank + 1) * S_own)
             sts, sus = st_all[own], su_all[own]
         elif world > 1:
-            dist.reduce_scatter_tensor(H_own, tr.H)
-            dist.reduce_scatter_tensor(D_own, tr.Dir)
+            nccl_ex.reduce_scatter(tr.H, H_own)
+            nccl_ex.reduce_scatter(tr.Dir, D_own)
             dist.reduce_scatter_tensor(st_own, tr.stats)
             dist.reduce_scatter_tensor(su_own, tr.sum_t)
             hs, ds, sts, sus = H_own, D_own, st_own, su_own
@@ -420,6 +424,8 @@ def run_gpu(args, w, metric, unit):
     if world > 1:
         if fused:
             peers.close()
+        else:
+            nccl_ex.close()
         dist.barrier()
         dist.destroy_process_group()   # every rank tears NCCL down before exit
     if rank != 0:

@@ -39,6 +39,7 @@ extern "C" {
 #define EF_ECUDA (-2)
 #define EF_ENOMEM (-3)
 #define EF_EUNSUPPORTED (-4)
+#define EF_ENCCL (-5)
 
 #define EF_ABI_VERSION 1
 
@@ -251,6 +252,29 @@ int ef_peer_free(void* dev_ptr);
 int ef_peer_open(const void* ipc_handle, void** dev_ptr);
 int ef_peer_close(void* dev_ptr);
 
+/* ---- unfused histogram exchange over NCCL -------
+ * Replaces the reference-side reduction of per-worker partial IRs (the
+ * paper's multi-threaded tracer sums per-thread IRs; SPEC.md:247-248 splits
+ * a frame over primary rays).  Rank g traces rays [g R/N, (g+1) R/N) of every
+ * source into local partial histograms with ef_trace; ef_nccl_reduce_hist
+ * then sums them:
+ *   EF_NCCL_REDUCE_SCATTER  partial = N * owned_count f32 (sources ordered
+ *                           by owner rank); owned = this rank's S/N sources,
+ *                           summed over ranks (K4 then runs on them);
+ *   EF_NCCL_ALLREDUCE       owned = sum of partial (owned_count f32; may alias);
+ *   EF_NCCL_REDUCE          the sum on rank 0.
+ * The communicator comes from ef_nccl_comm_create (unique id from
+ * ef_nccl_unique_id on one rank, shared out of band).  libnccl.so.2 is
+ * resolved at first use (dlopen); failures -> EF_ENCCL. */
+#define EF_NCCL_REDUCE_SCATTER 0
+#define EF_NCCL_ALLREDUCE 1
+#define EF_NCCL_REDUCE 2
+int ef_nccl_unique_id(uint8_t* out128);
+int ef_nccl_comm_create(int32_t world, int32_t rank, const uint8_t* id128, int32_t device, void** comm);
+int ef_nccl_comm_destroy(void* comm);
+int ef_nccl_reduce_hist(void* comm, const float* partial, float* owned, int64_t owned_count, int32_t mode,
+                        void* stream);
+
 /* ---- ir-analysis ------------------------------------------------------
  * Replaces estimate_rt60, reverb_gain (290),
  * estimate_predelay (299), average_directivity (308) and
@@ -310,6 +334,14 @@ int ef_audio_create(const ef_audio_config* cfg, const float* sos, const float* Y
                     const int32_t* p_int, const float* p_w, const int32_t* fdn_delay,
                     const float* g_line, const float* M, const float* hrtf_spec, ef_audio** out);
 int ef_audio_destroy(ef_audio* audio);
+/* update_params: swap the per-source parameters at a block
+ * boundary -- HOST arrays laid out as in ef_audio_create (NULL = keep):
+ * Y, d_int/d_w, gain, p_int/p_w, g_line, M.  Stream-ordered on `stream`
+ * (blocks enqueued before render with the old values); returns after the
+ * copies complete.  Line delays and HRTF are fixed at create. */
+int ef_audio_update(ef_audio* audio, const float* Y, const int32_t* d_int, const float* d_w,
+                    const float* gain, const int32_t* p_int, const float* p_w, const float* g_line,
+                    const float* M, void* stream);
 /* out[0]=n_sources out[1]=device bytes out[2]=next sample index out[3]=grid */
 int ef_audio_info(const ef_audio* audio, int64_t* out4);
 int ef_audio_process(ef_audio* audio, const float* x, float* bus_out, float* out, void* stream);

@@ -93,6 +93,19 @@ class AudioOracle:
         self.hrtf = hrtf                                # (16, 2, taps)
         self.bus_hist = np.zeros((16, 0))
 
+    def update(self, p: dict):
+        """update_params at a block boundary: new direct / reverb parameters
+        (line delays and HRTF unchanged), state carried over."""
+        q = dict(self.p)
+        for k in ("dir_direct", "delay_direct", "gain_direct", "predelay", "rt60", "g_reverb", "D"):
+            q[k] = p[k]
+        self.p = q
+        self.Y = eval_sh3(q["dir_direct"])
+        E = eval_sh3(line_directions()).T * np.sqrt(4.0 * np.pi / N_LINES)
+        m = q["fdn_delay"].astype(np.float64)
+        self.g_line = 10.0 ** (-3.0 * m[:, None, :] / (FS * q["rt60"][:, :, None]))
+        self.M = q["g_reverb"][:, :, None, None] * np.einsum("sbkj,ji->sbki", q["D"], E)
+
     @staticmethod
     def tap(hist, start, delay):
         """Linear fractional read of samples [start, start+BLOCK) delayed by

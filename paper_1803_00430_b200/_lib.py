@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EF_LIB_PATH", os.path.join(HERE, "libechoforge_b200.so"))
 
-EF_OK, EF_EINVAL, EF_ECUDA, EF_ENOMEM, EF_EUNSUPPORTED = 0, -1, -2, -3, -4
+EF_OK, EF_EINVAL, EF_ECUDA, EF_ENOMEM, EF_EUNSUPPORTED, EF_ENCCL = 0, -1, -2, -3, -4, -5
 ST_NAMES = ("paths", "segments", "reflections", "arrivals", "direct", "dropped", "escaped",
             "nodes", "tris")
 EF_ST_COUNT = 10
@@ -56,9 +56,10 @@ class AnalysisConfig(ctypes.Structure):
 EXPORTS = ("ef_abi_version", "ef_last_error", "ef_launch_count", "ef_scene_create",
            "ef_scene_destroy", "ef_scene_info", "ef_intersect_batch", "ef_occluded_batch",
            "ef_ray_triangles", "ef_eval_sh_batch", "ef_loudness_batch", "ef_trace", "ef_analyze", "ef_blend",
-           "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process",
+           "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process", "ef_audio_update",
            "ef_scene_refit", "ef_acoustic_metrics", "ef_scene_create_ex", "ef_scene_rebuild",
-           "ef_trace_fused", "ef_peer_alloc", "ef_peer_free", "ef_peer_open", "ef_peer_close")
+           "ef_trace_fused", "ef_peer_alloc", "ef_peer_free", "ef_peer_open", "ef_peer_close",
+           "ef_nccl_unique_id", "ef_nccl_comm_create", "ef_nccl_comm_destroy", "ef_nccl_reduce_hist")
 
 
 def lib():
@@ -103,6 +104,11 @@ def lib():
     L.ef_audio_destroy.argtypes = [vp]
     L.ef_audio_info.argtypes = [vp, vp]
     L.ef_audio_process.argtypes = [vp, vp, vp, vp, vp]
+    L.ef_audio_update.argtypes = [vp] * 10
+    L.ef_nccl_unique_id.argtypes = [vp]
+    L.ef_nccl_comm_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(vp)]
+    L.ef_nccl_comm_destroy.argtypes = [vp]
+    L.ef_nccl_reduce_hist.argtypes = [vp, vp, vp, i64, i32, vp]
     for name in EXPORTS:
         getattr(L, name).restype = ctypes.c_int if name != "ef_launch_count" else ctypes.c_uint64
     _lib = L

@@ -481,6 +481,39 @@ extern "C" int ef_audio_create(const ef_audio_config* cfg, const float* sos, con
     return EF_OK;
 }
 
+// Parameter swap at a block boundary (SPEC.md:415-420 update_params): the
+// given HOST arrays (NULL = keep) are copied on `stream`, so blocks enqueued
+// before this call render with the old parameters and later ones with the
+// new.  The FDN line delays and the HRTF are properties of the renderer and
+// stay; the band histories, line rings and filter states carry over.
+extern "C" int ef_audio_update(ef_audio* h, const float* Y, const int32_t* d_int, const float* d_w,
+                               const float* gain, const int32_t* p_int, const float* p_w,
+                               const float* g_line, const float* M, void* stream) {
+    if (!h) return set_error(EF_EINVAL, "ef_audio_update: null renderer");
+    AudioState& A = h->A;
+    const int S = A.S;
+    for (int s = 0; s < S; ++s) {
+        if ((d_int && (d_int[s] < 0 || d_int[s] + 2 + kBlock > A.hist_len)) ||
+            (p_int && (p_int[s] < 0 || p_int[s] + 2 + kBlock > A.hist_len)))
+            return set_error(EF_EINVAL, "ef_audio_update: direct delay / predelay outside the history ring");
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (src && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+    };
+    cp(A.Y, Y, (size_t)S * kSh * 4);
+    cp(A.d_int, d_int, (size_t)S * 4);
+    cp(A.d_w, d_w, (size_t)S * 4);
+    cp(A.gain, gain, (size_t)S * kBands * 4);
+    cp(A.p_int, p_int, (size_t)S * 4);
+    cp(A.p_w, p_w, (size_t)S * 4);
+    cp(A.g, g_line, (size_t)S * kBands * kLines * 4);
+    cp(A.M, M, (size_t)S * kBands * kSh * kLines * 4);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // the host arrays may be freed on return
+    return e == cudaSuccess ? EF_OK : check_cuda(e, "ef_audio_update");
+}
+
 extern "C" int ef_audio_destroy(ef_audio* h) {
     free_audio(h);
     return EF_OK;

@@ -1,0 +1,24 @@
+// Trace-kernel instantiations: all-pairs (lane-group) kernels
+// for 8-band scenes (see ef_trace_kernels.cuh).  One translation unit per
+// family so the build compiles them in parallel.
+#include "ef_trace_kernels.cuh"
+
+namespace ef {
+
+cudaError_t trace_dispatch_brute_nb8(int order, const TraceParams& P, cudaStream_t st) {
+    return dispatch_brute<8>(order, P, st);
+}
+
+#ifdef EF_PROFILE_PHASES
+void debug_phases_brute_nb8(unsigned long long* acc, int reset) {
+    unsigned long long v[12];
+    cudaMemcpyFromSymbol(v, g_phase, sizeof v);
+    for (int i = 0; i < 12; ++i) acc[i] += v[i];
+    if (reset) {
+        unsigned long long z[12] = {0};
+        cudaMemcpyToSymbol(g_phase, z, sizeof z);
+    }
+}
+#endif
+
+}  // namespace ef

@@ -1,19 +1,32 @@
 """Multi-GPU plumbing for the trace path.
 
-Paths are independent, so rays shard by global index: rank g traces rays
-[g*R, (g+1)*R) of every source with the same Philox streams as a single-GPU
-run.  The only exchange is the per-frame histogram sum, done with one
-reduce-scatter over the source axis so that each rank ends up owning the
-complete histograms of S/N sources (NCCL over NVLink on the B200 box; gloo
-for the CPU tests, which lacks reduce_scatter_tensor and falls back to
-all_reduce + slice).
+Paths are independent, so rays shard by global index: of a frame of R rays
+per source, rank g of N traces rays [g*R/N, (g+1)*R/N) of every source with
+the same Philox streams as a single-GPU run (strong scaling: the frame is
+fixed).  The only exchange is the per-frame histogram sum, so that each rank
+ends up owning the complete histograms of S/N sources:
+
+* fused (default): ef_trace_fused commits every splat straight into the
+  owner's block over peer memory (PeerHistograms below);
+* unfused: local partials (ef_trace) + one reduce-scatter -- torch's
+  (reduce_scatter_sources; gloo for the CPU tests, which lacks
+  reduce_scatter_tensor and falls back to all_reduce + slice) or the C ABI's
+  ef_nccl_reduce_hist (NcclHistExchange).
 """
 from __future__ import annotations
 
+import ctypes
 
-def shard_rays(rays_per_rank: int, rank: int):
-    """(ray0, n_rays) of this rank's slice (weak scaling: fixed per rank)."""
-    return rank * rays_per_rank, rays_per_rank
+
+def shard_rays(rays_per_source: int, rank: int, world: int):
+    """(ray0, n_rays) of this rank's slice of a frame of `rays_per_source`
+    rays per source (strong scaling)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    if rays_per_source % world:
+        raise ValueError(f"{rays_per_source} rays per source do not divide over {world} ranks")
+    per = rays_per_source // world
+    return rank * per, per
 
 
 def owned_sources(n_sources: int, rank: int, world: int):
@@ -240,3 +253,66 @@ class EmulatedPeers:
 
     def end_frame(self):
         pass
+
+
+# --------------------------------------------------------------------------
+# Unfused exchange through the C ABI's NCCL entry points (ef_nccl_*)
+class NcclHistExchange:
+    """ef_nccl_reduce_hist over a communicator made by ef_nccl_comm_create:
+    rank 0's unique id travels over torch.distributed (any backend) when
+    world > 1.  ``reduce_scatter(partial, owned)``: partial (S, ...) f32
+    device tensor of this rank's ray shard, owned (S/N, ...) this rank's
+    summed sources; ``all_reduce(buf)`` in place; ``reduce(buf)`` to rank 0."""
+
+    def __init__(self, world: int | None = None, rank: int | None = None, device: int | None = None):
+        from . import _lib
+        t = _lib.torch()
+        if world is None or rank is None:
+            import torch.distributed as dist
+            world, rank = dist.get_world_size(), dist.get_rank()
+        self.world, self.rank = int(world), int(rank)
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().ef_nccl_unique_id(uid))
+        if self.world > 1:
+            import torch.distributed as dist
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0)
+            ctypes.memmove(uid, box[0], 128)
+        dev = t.cuda.current_device() if device is None else int(device)
+        comm = ctypes.c_void_p()
+        _lib.check(_lib.lib().ef_nccl_comm_create(self.world, self.rank, uid, dev, ctypes.byref(comm)))
+        self._comm = comm
+
+    def _run(self, partial, owned, count, mode, stream):
+        from . import _lib
+        t = _lib.torch()
+        for x in (partial, owned):
+            if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float32 and x.is_contiguous()):
+                raise ValueError("NcclHistExchange: contiguous float32 CUDA tensors expected")
+        _lib.check(_lib.lib().ef_nccl_reduce_hist(self._comm, _lib.ptr(partial), _lib.ptr(owned), count, mode,
+                                                  _lib.stream_handle(stream)))
+
+    def reduce_scatter(self, partial, owned, stream=None):
+        if partial.shape[0] % self.world or owned.numel() * self.world != partial.numel():
+            raise ValueError("NcclHistExchange.reduce_scatter: owned must hold 1/world of partial")
+        self._run(partial, owned, owned.numel(), 0, stream)
+
+    def all_reduce(self, buf, stream=None):
+        self._run(buf, buf, buf.numel(), 1, stream)
+
+    def reduce(self, buf, out=None, stream=None):
+        out = buf if out is None else out
+        self._run(buf, out, buf.numel(), 2, stream)
+
+    def close(self):
+        from . import _lib
+        if getattr(self, "_comm", None) is not None and self._comm.value:
+            _lib.check(_lib.lib().ef_nccl_comm_destroy(self._comm))
+        self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

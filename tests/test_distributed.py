@@ -39,7 +39,7 @@ def _worker(rank, world, port, n, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     w = workloads.c1_shoebox()
     w.sources = np.array([[2.0, 2.0, 1.5], [3.0, 6.0, 1.0]])
-    ray0, nr = distributed.shard_rays(n, rank)
+    ray0, nr = distributed.shard_rays(world * n, rank, world)
     H, st = _oracle_frame(w, [0, 1], ray0, nr)
     Hr = distributed.reduce_scatter_sources(torch.from_numpy(H))
     Sr = distributed.reduce_scatter_sources(torch.from_numpy(st))
@@ -132,7 +132,7 @@ def _fused_worker(rank, world, port, n, tmpdir, q):
     for frame in (0, 1, 2):
         peers.begin_frame(frame)
         tab_h, _ = peers.tables(frame)
-        ray0, nr = distributed.shard_rays(n, rank)
+        ray0, nr = distributed.shard_rays(world * n, rank, world)
         from oracle import oracle as O
         os_ = O.OracleScene.from_arrays(w.arrays())
         for turn in range(world):                       # one writer at a time (no CPU atomics)
