@@ -86,9 +86,16 @@ def analyze(tracer, max_rt: float | None = None, loudness: bool = True) -> list[
 
 
 def _single_band(ir_band, sample_rate, max_rt):
-    """Run K4 on one intensity histogram (order 0, one band)."""
+    """Run K4 on one intensity histogram (order 0, one band).  K4 reads f32
+    histograms (the device accumulates in f32); the series is first scaled
+    by a power of two (exact) that maps its maximum into [1, 2), so every
+    non-zero bin stays non-zero in f32 unless it is below 2^-149 of the
+    maximum (only estimate_predelay uses this path; RT60 takes the f64 one)."""
     t = _lib.torch()
     I = np.asarray(ir_band, dtype=np.float64).reshape(-1)
+    peak = float(np.max(np.abs(I))) if I.size else 0.0
+    if peak > 0.0 and np.isfinite(peak):
+        I = I * 2.0 ** (-math.floor(math.log2(peak)))
     dev = _lib.device()
     H = t.as_tensor((I * SH_C0).astype(np.float32), device=dev).reshape(1, -1, 1, 1).contiguous()
     Dir = t.zeros((1, 1, 1), dtype=t.float32, device=dev)
@@ -102,9 +109,14 @@ def _single_band(ir_band, sample_rate, max_rt):
 def estimate_rt60(ir_band, sample_rate: float = 100.0, max_rt: float = 8.0):
     """RT60 (s) of an intensity histogram, or None when silent/indeterminate
     (SPEC.md:272-280): Schroeder backward integration from the last non-zero
-    bin, LS fit over -5..-35 dB (fallback -5..-25 dB), clamp [0.05, max_rt]."""
-    r = _single_band(ir_band, sample_rate, max_rt)
-    return None if r.silent_bands[0] else float(r.rt60[0])
+    bin, LS fit over -5..-35 dB (fallback -5..-25 dB), clamp [0.05, max_rt].
+    The caller's f64 series goes to the device as f64: the same Schroeder fit
+    as K4 (schroeder_fit, csrc/ef_analyze.cu) through ef_acoustic_metrics."""
+    I = np.asarray(ir_band, dtype=np.float64).reshape(-1)
+    if I.size == 0:
+        return None
+    rt = acoustic_metrics(I, 1.0 / sample_rate, max_rt=max_rt)["rt60"]
+    return None if rt < 0 else float(rt)
 
 
 def estimate_predelay(intensity, sample_rate: float = 100.0):

@@ -344,6 +344,14 @@ def test_spec_known_answers():
         assert abs(analysis.estimate_rt60(10 ** (-6 * tt / rt), fs) - rt) / rt < 0.02
     # scale invariance
     assert abs(analysis.estimate_rt60(7.0 * I, fs) - analysis.estimate_rt60(I, fs)) < 1e-6
+    # the caller's f64 series reaches the fit as f64: a series below the f32
+    # range (1e-300) gives the f64 oracle's answer, not "silent"
+    tiny = 1e-300 * I
+    ref_rt = OA.rt60_fit(tiny, 1.0 / fs, 8.0)[0]
+    assert analysis.estimate_rt60(tiny, fs) == pytest.approx(ref_rt, rel=1e-9)
+    z = np.zeros(50)
+    z[7], z[20] = 1e-300, 1.0e-290
+    assert analysis.estimate_predelay(z, fs) == pytest.approx(0.07)
     assert abs(analysis.reverb_gain(1.0 / (6 * np.log(10)), 1.0) - 1.0) < 1e-12
     assert abs(analysis.reverb_gain(4.0 / (6 * np.log(10)), 1.0) - 2.0) < 1e-12
     assert abs(1.0 / (6 * np.log(10)) - 0.072382) < 1e-6
