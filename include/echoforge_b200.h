@@ -252,6 +252,21 @@ int ef_peer_free(void* dev_ptr);
 int ef_peer_open(const void* ipc_handle, void** dev_ptr);
 int ef_peer_close(void* dev_ptr);
 
+/* ---- scene ingestion --------------------------
+ * Replaces _parse_obj (scene.py:255-280): positions only, fan triangulation,
+ * 1-based / negative indices, the current g / o / usemtl name per triangle;
+ * numbers parsed like Python's float() / int().  Malformed lines and
+ * out-of-range indices -> EF_EINVAL with file:line.  ef_mesh_info: out4 =
+ * n_verts, n_tris, n_groups, bytes of the NUL-separated group names;
+ * ef_mesh_arrays fills HOST verts (V,3) f64, tris (T,3) i64 0-based,
+ * tri_group (T) i32 and the names (any pointer may be NULL). */
+typedef struct ef_mesh ef_mesh;
+int ef_obj_parse(const char* path, ef_mesh** out);
+int ef_mesh_info(const ef_mesh* mesh, int64_t* out4);
+int ef_mesh_arrays(const ef_mesh* mesh, double* verts, int64_t* tris, int32_t* tri_group, char* names,
+                   int64_t names_bytes);
+int ef_mesh_destroy(ef_mesh* mesh);
+
 /* ---- unfused histogram exchange over NCCL -------
  * Replaces the reference-side reduction of per-worker partial IRs (the
  * paper's multi-threaded tracer sums per-thread IRs; SPEC.md:247-248 splits

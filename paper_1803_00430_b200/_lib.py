@@ -59,7 +59,8 @@ EXPORTS = ("ef_abi_version", "ef_last_error", "ef_launch_count", "ef_scene_creat
            "ef_audio_create", "ef_audio_destroy", "ef_audio_info", "ef_audio_process", "ef_audio_update",
            "ef_scene_refit", "ef_acoustic_metrics", "ef_scene_create_ex", "ef_scene_rebuild",
            "ef_trace_fused", "ef_peer_alloc", "ef_peer_free", "ef_peer_open", "ef_peer_close",
-           "ef_nccl_unique_id", "ef_nccl_comm_create", "ef_nccl_comm_destroy", "ef_nccl_reduce_hist")
+           "ef_nccl_unique_id", "ef_nccl_comm_create", "ef_nccl_comm_destroy", "ef_nccl_reduce_hist",
+           "ef_obj_parse", "ef_mesh_info", "ef_mesh_arrays", "ef_mesh_destroy")
 
 
 def lib():
@@ -109,6 +110,10 @@ def lib():
     L.ef_nccl_comm_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(vp)]
     L.ef_nccl_comm_destroy.argtypes = [vp]
     L.ef_nccl_reduce_hist.argtypes = [vp, vp, vp, i64, i32, vp]
+    L.ef_obj_parse.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.ef_mesh_info.argtypes = [vp, vp]
+    L.ef_mesh_arrays.argtypes = [vp, vp, vp, vp, vp, i64]
+    L.ef_mesh_destroy.argtypes = [vp]
     for name in EXPORTS:
         getattr(L, name).restype = ctypes.c_int if name != "ef_launch_count" else ctypes.c_uint64
     _lib = L
