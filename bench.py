@@ -484,6 +484,119 @@ def run_gpu(args, w, metric, unit):
     print(json.dumps(line), flush=True)
 
 
+def run_inflight(args, w, metric, unit):
+    """Frames in flight (one GPU, static configs): F FrameTracer/Analyzer
+    sets on F streams, frame i on set i % F, so frame i+1's trace kernel
+    takes the SMs that frame i's tail releases (C2: one 100-bounce path keeps
+    ~1/3 of a lone frame busy on one SM).  Throughput = all
+    segments / the span of the K timed frames (CUDA events); per-frame
+    latency = each frame's own start -> end events.  The L2 is not flushed
+    between frames here (they overlap); the C2 scene (0.3 MB) is L1/L2
+    resident either way.  e2e repeats with per-frame host copies (source
+    positions in; LowRateIR + parameters out, pinned, per slot)."""
+    import torch
+
+    from paper_1803_00430_b200 import _lib
+    from paper_1803_00430_b200.analysis import Analyzer
+    from paper_1803_00430_b200.propagation import FrameTracer, TraceConfig
+    from paper_1803_00430_b200.scene import scene_from_workload
+
+    world, rank, local = dist_env()
+    if world != 1:
+        raise SystemExit("--inflight is a single-GPU mode")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    F = args.inflight
+    sc = scene_from_workload(w)
+    S = len(w.sources)
+    cfg = TraceConfig(primary_rays=w.n_rays, max_order=w.max_bounces, sh_order=w.order,
+                      bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    slots = []
+    for _ in range(F):
+        tr = FrameTracer(sc, S, cfg)
+        tr.set_sources(w.sources)
+        an = Analyzer(S, w.n_bins, sc.n_bands, w.order, w.bin_s)
+        host = {"src": torch.from_numpy(np.ascontiguousarray(w.sources, np.float64)).pin_memory(),
+                "H": torch.empty(tuple(tr.H.shape), dtype=torch.float32).pin_memory(),
+                "D": torch.empty(tuple(tr.Dir.shape), dtype=torch.float32).pin_memory(),
+                "P": torch.empty(tuple(an.params.shape), dtype=torch.float64).pin_memory(),
+                "Q": torch.empty(tuple(an.src_params.shape), dtype=torch.float64).pin_memory()}
+        slots.append((torch.cuda.Stream(), tr, an, host, torch.zeros((), dtype=torch.int64, device=dev)))
+    nf = max(w.n_frames, 1)
+
+    def frame(i, ev=None, e2e=False):
+        st, tr, an, host, segs = slots[i % F]
+        with torch.cuda.stream(st):
+            if ev is not None:
+                ev[0].record(st)
+            if e2e:
+                tr.src_pos.copy_(host["src"], non_blocking=True)
+            tr.trace(w.listener, frame=i % nf, stream=st)
+            an.run(tr.H, tr.Dir, tr.stats, tr.sum_t, stream=st)
+            if e2e:
+                host["H"].copy_(tr.H, non_blocking=True)
+                host["D"].copy_(tr.Dir, non_blocking=True)
+                host["P"].copy_(an.params, non_blocking=True)
+                host["Q"].copy_(an.src_params, non_blocking=True)
+            if ev is not None:
+                ev[1].record(st)
+            segs.add_(tr.stats[:, 1].sum())
+
+    def timed(e2e):
+        for i in range(args.warmup):
+            frame(i, e2e=e2e)
+        torch.cuda.synchronize()
+        for sl in slots:
+            sl[4].zero_()
+        main = torch.cuda.current_stream()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        t0.record(main)
+        for sl in slots:
+            sl[0].wait_event(t0)
+        for i in range(args.steps):
+            frame(args.warmup + i, evs[i], e2e)
+        for sl in slots:
+            main.wait_stream(sl[0])
+        t1.record(main)
+        torch.cuda.synchronize()
+        span = t0.elapsed_time(t1)
+        lat = [a.elapsed_time(b) for a, b in evs]
+        segs = sum(int(sl[4].item()) for sl in slots)
+        return span, lat, segs
+
+    n0 = _lib.launch_count()
+    with ClockSampler(local) as clocks:
+        span, lat, segs = timed(False)
+    n_launch = _lib.launch_count() - n0 - args.warmup * 2   # the warm-up frames' trace + analysis
+    e_span, e_lat, e_segs = timed(True)
+    st0, tr0, an0, host0, _ = slots[0]
+    h2d = host0["src"].numel() * 8
+    d2h = host0["H"].numel() * 4 + host0["D"].numel() * 4 + host0["P"].numel() * 8 + host0["Q"].numel() * 8
+    value = segs / (span * 1e-3)
+    peak, peak_kind = measured_peaks()
+    bseg = b_seg(args.config, sc.n_bands, cfg.n_coeffs)
+    achieved = bseg * segs / (span * 1e-3) / 1e9
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": span / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_block(args, w, 1), frames_in_flight=F,
+                           l2="not flushed: frames overlap (scene L1/L2-resident)"),
+            "e2e": {"value": e_segs / (e_span * 1e-3), "unit": unit, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e_span / args.steps},
+            "gpu_launches": int(n_launch),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                         "kernel": "trace_kernel + tail_kernel (frames overlapped; span time)",
+                         "algorithmic_bytes_per_segment": bseg},
+            "frame_latency_ms": {q: float(np.percentile(lat, p)) for q, p in
+                                 (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))},
+            "segments_per_step": segs / args.steps, "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def run_c4(args):
     """C4: sources rendered per 512-sample block within the 10.667 ms
     deadline (BASELINE configs[3]).  Sweeps S geometrically, then bisects
@@ -656,6 +769,8 @@ def main():
                          "memory (fused) or a separate NCCL reduce-scatter")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: several ranks on one GPU for plumbing checks (fused only)")
+    ap.add_argument("--inflight", type=int, default=1,
+                    help="frames in flight on separate streams (single GPU, static configs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum wall time of the CPU baseline sample")
     args = ap.parse_args()
@@ -675,6 +790,10 @@ def main():
     unit = "segments/s"
     if args.impl == "reference":
         run_reference(args, w, metric, unit)
+    elif args.inflight > 1:
+        if w.n_frames > 1 and w.source_velocity is not None:
+            raise SystemExit("--inflight needs a static config (C3's frames are sequential)")
+        run_inflight(args, w, metric, unit)
     else:
         run_gpu(args, w, metric, unit)
 
