@@ -355,8 +355,13 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         const int max_stack = 3 * s->max_depth + 1;
         const size_t sstack_bytes = (size_t)max_stack * kSmallThreads * sizeof(uint2) +
                                     (size_t)ns * (EF_ST_COUNT * 4 + 8) + 64;
-        P.smem_stack = (!brute && !big && sstack_env && max_stack <= kStackSize &&
-                        sstack_bytes <= kMaxSstackBytes) ? max_stack : 0;
+        static const size_t sstack_max = [] {   // tuning: shared-stack budget (KB)
+            const char* e = std::getenv("EF_SSTACK_MAXKB");
+            return e ? (size_t)std::atoi(e) * 1024 : kMaxSstackBytes;
+        }();
+        const bool sstack_fits = max_stack <= kStackSize && sstack_bytes <= sstack_max;
+        P.smem_stack = (!brute && (!big || sstack_max != kMaxSstackBytes) && sstack_env && sstack_fits)
+                           ? max_stack : 0;
         if (s->n_bands <= 4) {
             e = brute ? trace_dispatch_brute_nb4(cfg->order, P, st)
                       : trace_dispatch_bvh_nb4(big, cfg->order, P, st);

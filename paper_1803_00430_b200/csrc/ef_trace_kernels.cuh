@@ -678,8 +678,30 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         // __all_sync(!active) exit -- the compiler lays the loop out better)
         const unsigned live = __ballot_sync(kFull, S.active);
         if (!live) break;
+#ifndef EF_PROFILE_PHASES
         if (!S.active) continue;
         trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, s_tri, s_stack, lg);
+#else
+        const uint32_t n0 = ls.c[EF_ST_NODES], t0 = ls.c[EF_ST_TRIS];
+        const bool was = S.active;
+        if (S.active) trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, s_tri, s_stack, lg);
+        {   // SIMT cost of per-lane traversal lengths: 5 sum of node visits,
+            // 6 sum over warp-segments of max visits x 32, 7 the same for
+            // triangle tests (8 their sum), 9 segments (active lanes)
+            const uint32_t dn = was ? ls.c[EF_ST_NODES] - n0 : 0u, dt = was ? ls.c[EF_ST_TRIS] - t0 : 0u;
+            const uint32_t sn = __reduce_add_sync(kFull, dn), mn = __reduce_max_sync(kFull, dn);
+            const uint32_t st = __reduce_add_sync(kFull, dt), mt = __reduce_max_sync(kFull, dt);
+            const uint32_t na = __popc(__ballot_sync(kFull, was));
+            if (lane == 0) {
+                atomicAdd(&g_phase[5], (unsigned long long)sn);
+                atomicAdd(&g_phase[6], 32ull * mn);
+                atomicAdd(&g_phase[7], 32ull * mt);
+                atomicAdd(&g_phase[8], (unsigned long long)st);
+                atomicAdd(&g_phase[9], (unsigned long long)na);
+            }
+        }
+        if (!was) continue;
+#endif
         fin = !S.active;
     }
     if (lg.lead) flush_stats(ls, s_stats, s_sumt);
@@ -997,8 +1019,8 @@ static cudaError_t dispatch_brute(int order, const TraceParams& P, cudaStream_t 
 
 template <int NBMAX>
 static cudaError_t dispatch_bvh(bool big, int order, const TraceParams& P, cudaStream_t st) {
-    if (big) return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
     if (P.smem_stack > 0) return dispatch_order<NBMAX, false, kSmallThreads, 1, true>(order, P, st);
+    if (big) return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
     return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
 }
 
