@@ -641,11 +641,13 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         const unsigned mask = __ballot_sync(kFull, need && lg.lead);
         if (mask) {
             const int leader = __ffs(mask) - 1;
+            const unsigned rank = __popc(mask & ((1u << lg.gbase) - 1u));
+            unsigned long long my;
             unsigned long long base = 0;
             if (lane == leader) base = atomicAdd(P.counter, (unsigned long long)__popc(mask));
-            base = __shfl_sync(kFull, base, leader);
+            my = __shfl_sync(kFull, base, leader) + rank;
             if (need) {
-                S.path = base + __popc(mask & ((1u << lg.gbase) - 1u));
+                S.path = my;
                 if (S.path >= P.total) {
                     exhausted = true;
                 } else {

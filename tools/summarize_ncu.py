@@ -28,7 +28,27 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        # L1/TEX and L2 (the big-scene kernel is L1/TEX-bound)
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_output_wavefronts_pipe_lsu_mem_local_op_ld.sum",
+        "l1tex__t_output_wavefronts_pipe_lsu_mem_local_op_st.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "derived__memory_l2_theoretical_sectors_global_excessive",
+        "derived__memory_l1_wavefronts_shared_excessive",
+        "l1tex__m_l1tex2xbar_write_sectors_mem_lg_op_st.sum",
+        # histogram commits (red) and the path counter (atom)
+        "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum",
+        "smsp__inst_executed_op_global_red.sum",
+        "lts__t_requests_srcunit_tex_op_red.sum",
+        "smsp__average_warp_latency_per_inst_issued.ratio"]
 
 
 def launches(path):
