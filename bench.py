@@ -626,9 +626,17 @@ def run_c4(args):
                 out[k] = v
         return out
 
+    # the configured input: seeded pink noise (workloads.pink_noise), 64
+    # distinct source signals tiled over S sources, one 512-sample block
+    pink = torch.from_numpy(workloads.pink_noise(64, 3 * 512))
+
+    def pink_block(S, k=0):
+        reps = (S + 63) // 64
+        return pink[:, k * 512:(k + 1) * 512].repeat(reps, 1)[:S].contiguous()
+
     def measure(S, steps):
         r = render.SHRenderer(params(S))
-        x = torch.randn((S, 512), dtype=torch.float32, device=dev) * 0.1
+        x = pink_block(S).to(dev)
         for _ in range(args.warmup):
             r.process(x, want_bus=False)
         torch.cuda.synchronize()
@@ -647,7 +655,7 @@ def run_c4(args):
         # render, so the period is max(upload, render + read-back) and the
         # output is one block later.  Every upload and read-back is inside
         # the timed span (first upload to last read-back).
-        xh = [torch.randn((S, 512), dtype=torch.float32).pin_memory() for _ in range(2)]
+        xh = [pink_block(S, k).pin_memory() for k in (1, 2)]
         xd = [x, torch.empty_like(x)]
         oh = torch.empty((2, 512), dtype=torch.float32).pin_memory()
         main = torch.cuda.current_stream()

@@ -189,16 +189,45 @@ struct __align__(32) F8 {
 struct __align__(32) D4 {
     double x, y, z, w;
 };
+// L1 policy hints of the node / triangle loads: the triangle records
+// (tested ~3 per segment, rarely reused from L1) skip L1 allocation so the
+// node working set stays (C5 3.92 vs 3.88, C3 2.42 vs 2.40 G seg/s, r02t;
+// evict_first 3.87, evict_last on the nodes 3.88).  Tuning builds:
+// EF_NODE_HINT 1 = L1::evict_last; EF_TRI_HINT 0 = none, 1 = L1::no_allocate,
+// 2 = L1::evict_first
+#ifndef EF_NODE_HINT
+#define EF_NODE_HINT 0
+#endif
+#ifndef EF_TRI_HINT
+#define EF_TRI_HINT 1
+#endif
+#if EF_NODE_HINT == 1
+#define EF_NODE_Q ".L1::evict_last"
+#else
+#define EF_NODE_Q ""
+#endif
+#if EF_TRI_HINT == 1
+#define EF_TRI_Q ".L1::no_allocate"
+#elif EF_TRI_HINT == 2
+#define EF_TRI_Q ".L1::evict_first"
+#else
+#define EF_TRI_Q ""
+#endif
 __device__ __forceinline__ F8 ldg_f8(const void* p) {
     F8 r;
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc" EF_NODE_Q ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(r.a), "=f"(r.b), "=f"(r.c), "=f"(r.d), "=f"(r.e), "=f"(r.f), "=f"(r.g), "=f"(r.h)
         : "l"(p));
     return r;
 }
 __device__ __forceinline__ D4 ldg_d4(const void* p) {
     D4 r;
-    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    asm("ld.global.nc" EF_TRI_Q ".v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ldg_d2(const void* p) {
+    double2 r;
+    asm("ld.global.nc" EF_TRI_Q ".v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
     return r;
 }
 
@@ -352,7 +381,7 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
     for (uint32_t i = 0; i < cnt; ++i) {
         const GpuTri* q = tris + start + i;   // 96 bytes: three 256-bit loads
         const D4 a = ldg_d4(q->v), b = ldg_d4(q->v + 4);
-        const double2 c = __ldg(reinterpret_cast<const double2*>(q->v + 8));
+        const double2 c = ldg_d2(q->v + 8);
         const double v[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x};
         const int32_t id = (int32_t)__double_as_longlong(c.y);
         double t;

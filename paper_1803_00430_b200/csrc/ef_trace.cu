@@ -320,7 +320,11 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         }
         // vector reductions into this GPU's own blocks; scalar f32 reds over
         // the peer mapping (remote NVLink targets)
-        P.vec_red = fused ? 0 : 1;
+        static const int vec_env = [] {   // A/B: EF_VEC_RED=0 commits with scalar reds
+            const char* e = std::getenv("EF_VEC_RED");
+            return e ? std::atoi(e) : 1;
+        }();
+        P.vec_red = (fused || !vec_env) ? 0 : 1;
         P.stats = stats + (size_t)s0 * EF_ST_COUNT;
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;
