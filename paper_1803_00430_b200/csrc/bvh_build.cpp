@@ -65,6 +65,13 @@ double intersect_cost() {
     const char* e = std::getenv("EF_BVH_CI");
     return e ? std::atof(e) : 2.0;
 }
+// Leaves of at most this many triangles are never split (tuning:
+// EF_BVH_MINLEAF; 1 = pure SAH decision).
+int min_leaf() {
+    const char* e = std::getenv("EF_BVH_MINLEAF");
+    const int v = e ? std::atoi(e) : 1;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+}
 int max_leaf() {
     const char* e = std::getenv("EF_BVH_MAXLEAF");
     const int v = e ? std::atoi(e) : kMaxLeaf;
@@ -100,6 +107,7 @@ struct Builder {
     int64_t budget = 0;              // spatial-split duplications left
     const double kIntersectCost = intersect_cost();
     const int kLeafMax = ef::max_leaf();
+    const int kLeafMin = std::min(ef::min_leaf(), kLeafMax);
     const double kSplitAlpha = split_alpha();
 
     Builder(const double* a, const double* b, const double* c) : v0(a), e1(b), e2(c) {}
@@ -157,7 +165,7 @@ struct Builder {
         }
         if (depth == 0) root_area = box.half_area();
         const int64_t n = (int64_t)refs.size();
-        if (n == 1) return make_leaf(box, refs);
+        if (n <= kLeafMin) return make_leaf(box, refs);
         const double parent = std::max(box.half_area(), 1e-300);
         std::vector<Ref> L, R;
         bool split_found = false;
