@@ -602,6 +602,7 @@ def run_inflight(args, w, metric, unit):
         torch.cuda.synchronize()
         for sl in slots:
             sl[4].zero_()
+        n0 = _lib.launch_count()
         main = torch.cuda.current_stream()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -619,13 +620,11 @@ def run_inflight(args, w, metric, unit):
         span = t0.elapsed_time(t1)
         lat = [a.elapsed_time(b) for a, b in evs]
         segs = sum(int(sl[4].item()) for sl in slots)
-        return span, lat, segs
+        return span, lat, segs, _lib.launch_count() - n0
 
-    n0 = _lib.launch_count()
     with ClockSampler(local) as clocks:
-        span, lat, segs = timed(False)
-    n_launch = _lib.launch_count() - n0 - args.warmup * 2   # the warm-up frames' trace + analysis
-    e_span, e_lat, e_segs = timed(True)
+        span, lat, segs, n_launch = timed(False)
+    e_span, e_lat, e_segs, _ = timed(True)
     st0, tr0, an0, host0, _ = slots[0]
     h2d = host0["src"].numel() * 8
     d2h = host0["H"].numel() * 4 + host0["D"].numel() * 4 + host0["P"].numel() * 8 + host0["Q"].numel() * 8
