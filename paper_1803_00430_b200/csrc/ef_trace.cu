@@ -324,7 +324,11 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
             const char* e = std::getenv("EF_VEC_RED");
             return e ? std::atoi(e) : 1;
         }();
-        P.vec_red = (fused || !vec_env) ? 0 : 1;
+        // (the caller's H / Dir must start on 16-byte boundaries for the
+        // vector form; any other base falls back to scalar reds)
+        const bool aligned16 = !fused && (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
+                               (reinterpret_cast<uintptr_t>(Dir) % 16 == 0);
+        P.vec_red = (aligned16 && vec_env) ? 1 : 0;
         P.stats = stats + (size_t)s0 * EF_ST_COUNT;
         P.sum_t = sum_t + s0;
         P.path_nseg = path_nseg ? path_nseg + (size_t)s0 * cfg->n_rays : nullptr;

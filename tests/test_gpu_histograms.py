@@ -172,3 +172,27 @@ def test_c3_cached_histogram_and_estimators_vs_oracle():
         np.testing.assert_allclose(g.reverb_gain, ora["gain"], rtol=1e-2)
         assert g.predelay == ora["predelay"]
         np.testing.assert_allclose(g.loudness, ora["loudness"], rtol=1e-3, atol=1e-3 * np.abs(ora["loudness"]).max())
+
+
+def test_commit_with_misaligned_outputs():
+    """A caller's H / Dir off a 16-byte boundary take the scalar commit
+    (ef_trace checks the alignment): same histogram as the vector form."""
+    w = workloads.c1_shoebox()
+    sc = scene.scene_from_workload(w)
+    tr = propagation.FrameTracer(sc, 1, _cfg(w))
+    tr.set_sources(w.sources)
+    tr.trace(w.listener)
+    torch.cuda.synchronize()
+    Ha = tr.H.clone()
+    Da = tr.Dir.clone()
+    Hbuf = torch.zeros(tr.H.numel() + 1, dtype=torch.float32, device=tr.H.device)
+    Dbuf = torch.zeros(tr.Dir.numel() + 1, dtype=torch.float32, device=tr.H.device)
+    tr.H = Hbuf[1:].view(tuple(Ha.shape))
+    tr.Dir = Dbuf[1:].view(tuple(Da.shape))
+    assert tr.H.data_ptr() % 16 != 0
+    tr.trace(w.listener)
+    torch.cuda.synchronize()
+    assert int(tr.stats[0, 3]) > 0
+    hist_close(tr.H[0].cpu().numpy(), Ha[0].cpu().numpy())
+    np.testing.assert_allclose(tr.Dir.cpu().numpy(), Da.cpu().numpy(), rtol=1e-5,
+                               atol=1e-6 * float(Da.abs().max()))
