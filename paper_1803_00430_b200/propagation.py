@@ -373,9 +373,9 @@ def trace_frame(scene, source, listener, config: TraceConfig, caches: CoherenceC
     cfg = TraceConfig(**{**config.__dict__, "seed": seed})
     pos = source.pose_at(frame * (dt or 0.0)) if hasattr(source, "pose_at") else np.asarray(source)
     lpos = listener.pose_at(frame * (dt or 0.0))[0] if hasattr(listener, "pose_at") else np.asarray(listener)
-    key = 0
-    if hasattr(scene, "sources") and source in scene.sources:
-        key = scene.sources.index(source)
+    # the source's index in the scene keys its RNG stream and its IR cache
+    # entry (by identity: positions are arrays, so == is elementwise)
+    key = next((i for i, s in enumerate(getattr(scene, "sources", [])) if s is source), 0)
     if scene.n_triangles == 0:
         t = _lib.torch()
         dev = _lib.device()

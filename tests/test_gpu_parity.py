@@ -378,6 +378,35 @@ def test_accumulate_ir_kernel():
                                (al * b + (1 - al) * a).cpu().numpy(), rtol=1e-6)
 
 
+def test_trace_frame_cache_expiry_before_blend():
+    """An IR cache entry older than 2 tau_LR expires BEFORE the next frame is
+    blended: the returned IR is the frame's own, and the cache
+    then holds it."""
+    w = workloads.c1_shoebox()
+    sc = scene.scene_from_workload(w)
+    cfg = propagation.TraceConfig(primary_rays=1024, max_order=w.max_bounces, sh_order=w.order,
+                                  bin_s=w.bin_s, n_bins=w.n_bins, listener_radius=w.radius, seed=w.seed)
+    caches = propagation.CoherenceCaches()
+    src, lst = sc.sources[0], sc.listener
+    _, ir1, _ = propagation.trace_frame(sc, src, lst, cfg, caches, frame=0, dt=0.1)
+    _, ir2, _ = propagation.trace_frame(sc, src, lst, cfg, caches, frame=1, dt=0.1)
+    fresh2 = propagation.trace_frame(sc, src, lst, cfg, frame=1)[1]
+    a = 1.0 - np.exp(-0.1 / caches.tau_lr)
+    h1 = ir1.histogram.cpu().numpy().astype(np.float64)
+    expect = a * fresh2.histogram.cpu().numpy() + (1 - a) * h1
+    assert np.abs(h1).max() > 0
+    np.testing.assert_allclose(ir2.histogram.cpu().numpy(), expect, rtol=1e-5, atol=1e-6 * np.abs(h1).max())
+    # a long gap: the old entry expires first, so frame 2's IR is its own
+    _, ir3, _ = propagation.trace_frame(sc, src, lst, cfg, caches, frame=2, dt=3.0 * caches.tau_lr)
+    fresh3 = propagation.trace_frame(sc, src, lst, cfg, frame=2)[1]
+    # a bare position works too (no cache key lookup by value)
+    assert propagation.trace_frame(sc, np.array(w.sources[0]), lst, cfg, frame=2)[2].total_segments > 0
+    assert np.abs(fresh3.histogram.cpu().numpy()).sum() > 0
+    assert np.array_equal(ir3.histogram.cpu().numpy(), fresh3.histogram.cpu().numpy()) or \
+        np.allclose(ir3.histogram.cpu().numpy(), fresh3.histogram.cpu().numpy(), rtol=1e-5, atol=0)
+    assert 0 in caches.ir and caches.ir[0] is ir3
+
+
 def test_mean_free_path_shoebox():
     """10 m cube, >= 1e5 segments: mfp ~ 4V/S within 3%."""
     from paper_1803_00430_b200.workloads import Workload, box_triangles
