@@ -356,6 +356,69 @@ __device__ __forceinline__ uint32_t slab_key(const RayF& r, float nx, float fx, 
     return tn <= tf ? ((__float_as_uint(tn) & ~3u) | slot) : 0xffffffffu;
 }
 
+// Packed f32x2 FMA (sm_100 FFMA2): two children's planes per instruction.
+// ptxas folds a pair {x, x} built from one scalar (with - and |.|) into the
+// instruction's scalar-broadcast operand, so the ray terms cost no registers.
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pack2(float a, float b) {
+    f32x2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void unpack2(f32x2_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2_t ffma2(f32x2_t a, f32x2_t b, f32x2_t c) {
+    f32x2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Slab distances of one axis for two children in the centre / half-extent
+// form (TravNode): m = c (1/d) - o/d, near = m - e |1/d|, far = m + e |1/d|.
+// Conservative like the lo/hi form: [c - e, c + e] encloses the padded box,
+// and the three roundings stay ~2^-23 of max(|c|, |o|, |e|) |1/d|, far below
+// the boxes' 1e-5 * scale padding.
+__device__ __forceinline__ void slab_ce2(float c0, float c1, float e0, float e1, float inv, float oinv,
+                                         float& n0, float& n1, float& f0, float& f1) {
+    const f32x2_t m = ffma2(pack2(c0, c1), pack2(inv, inv), pack2(-oinv, -oinv));
+    const f32x2_t e = pack2(e0, e1);
+    unpack2(ffma2(e, pack2(-fabsf(inv), -fabsf(inv)), m), n0, n1);
+    unpack2(ffma2(e, pack2(fabsf(inv), fabsf(inv)), m), f0, f1);
+}
+
+__device__ __forceinline__ uint32_t slab_key_ce(float nx, float fx, float ny, float fy, float nz, float fz,
+                                                float tmin, float tmax, uint32_t slot) {
+    const float tn = fmax3f(nx, ny, fmaxf(nz, tmin));
+    const float tf = fmin3f(fx, fy, fminf(fz, tmax));
+    return tn <= tf ? ((__float_as_uint(tn) & ~3u) | slot) : 0xffffffffu;
+}
+
+// The four children's sortable keys of one node visit (X, Y, Z: the node's
+// three 32-byte plane groups).
+__device__ __forceinline__ void node_keys(const RayF& r, const F8& X, const F8& Y, const F8& Z, float tmin,
+                                          float tmax, uint32_t& k0, uint32_t& k1, uint32_t& k2,
+                                          uint32_t& k3) {
+#if EF_SLAB_CE
+    float nx[4], fx[4], ny[4], fy[4], nz[4], fz[4];
+    slab_ce2(X.a, X.b, X.e, X.f, r.ix, r.ox, nx[0], nx[1], fx[0], fx[1]);
+    slab_ce2(X.c, X.d, X.g, X.h, r.ix, r.ox, nx[2], nx[3], fx[2], fx[3]);
+    slab_ce2(Y.a, Y.b, Y.e, Y.f, r.iy, r.oy, ny[0], ny[1], fy[0], fy[1]);
+    slab_ce2(Y.c, Y.d, Y.g, Y.h, r.iy, r.oy, ny[2], ny[3], fy[2], fy[3]);
+    slab_ce2(Z.a, Z.b, Z.e, Z.f, r.iz, r.oz, nz[0], nz[1], fz[0], fz[1]);
+    slab_ce2(Z.c, Z.d, Z.g, Z.h, r.iz, r.oz, nz[2], nz[3], fz[2], fz[3]);
+    k0 = slab_key_ce(nx[0], fx[0], ny[0], fy[0], nz[0], fz[0], tmin, tmax, 0u);
+    k1 = slab_key_ce(nx[1], fx[1], ny[1], fy[1], nz[1], fz[1], tmin, tmax, 1u);
+    k2 = slab_key_ce(nx[2], fx[2], ny[2], fy[2], nz[2], fz[2], tmin, tmax, 2u);
+    k3 = slab_key_ce(nx[3], fx[3], ny[3], fy[3], nz[3], fz[3], tmin, tmax, 3u);
+#else
+    k0 = slab_key_minmax(r, X.a, X.e, Y.a, Y.e, Z.a, Z.e, tmin, tmax, 0u);
+    k1 = slab_key_minmax(r, X.b, X.f, Y.b, Y.f, Z.b, Z.f, tmin, tmax, 1u);
+    k2 = slab_key_minmax(r, X.c, X.g, Y.c, Y.g, Z.c, Z.g, tmin, tmax, 2u);
+    k3 = slab_key_minmax(r, X.d, X.h, Y.d, Y.h, Z.d, Z.h, tmin, tmax, 3u);
+#endif
+}
+
 __device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
     a = lo;
@@ -482,7 +545,7 @@ __device__ __forceinline__ uint32_t stack_column(const uint2* s_stack) {
 // leaf, so the expensive f64 leaf tests of a warp run together.  The stack
 // (st, empty on entry) is one of the forms above.
 template <typename StackT>
-__device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
+__device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max, uint32_t& n_nodes, uint32_t& n_tris,
@@ -500,13 +563,11 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
             ++n_nodes;
 #endif
             // three 256-bit loads (lo/hi planes of x, y, z), one 128-bit (children)
-            const GpuNode* q = nodes + node;
-            const F8 X = ldg_f8(q->lox), Y = ldg_f8(q->loy), Z = ldg_f8(q->loz);
+            const TravNode* q = nodes + node;
+            const F8 X = ldg_f8(q->cx), Y = ldg_f8(q->cy), Z = ldg_f8(q->cz);
             const int4 ch = __ldg(reinterpret_cast<const int4*>(q->child));
-            uint32_t k0 = slab_key_minmax(r, X.a, X.e, Y.a, Y.e, Z.a, Z.e, tminf, tb, 0u);
-            uint32_t k1 = slab_key_minmax(r, X.b, X.f, Y.b, Y.f, Z.b, Z.f, tminf, tb, 1u);
-            uint32_t k2 = slab_key_minmax(r, X.c, X.g, Y.c, Y.g, Z.c, Z.g, tminf, tb, 2u);
-            uint32_t k3 = slab_key_minmax(r, X.d, X.h, Y.d, Y.h, Z.d, Z.h, tminf, tb, 3u);
+            uint32_t k0, k1, k2, k3;
+            node_keys(r, X, Y, Z, tminf, tb, k0, k1, k2, k3);
             kswap(k0, k1);
             kswap(k2, k3);
             kswap(k0, k2);
@@ -565,7 +626,7 @@ __device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
 // The trace kernels' forms: the whole stack in shared memory (SSTACK), or
 // its top DEPTH entries there and the rest in local memory; THREADS columns.
 template <int THREADS, int DEPTH, bool SSTACK>
-__device__ __forceinline__ Hit closest_bvh_column(const GpuNode* __restrict__ nodes,
+__device__ __forceinline__ Hit closest_bvh_column(const TravNode* __restrict__ nodes,
                                                   const GpuTri* __restrict__ tris, double ox,
                                                   double oy, double oz, double dx, double dy,
                                                   double dz, double t_min, double t_max,
@@ -581,7 +642,7 @@ __device__ __forceinline__ Hit closest_bvh_column(const GpuNode* __restrict__ no
     }
 }
 
-__device__ __forceinline__ Hit closest_bvh(const GpuNode* __restrict__ nodes,
+__device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                                            const GpuTri* __restrict__ tris, double ox, double oy,
                                            double oz, double dx, double dy, double dz, double t_min,
                                            double t_max) {

@@ -34,6 +34,23 @@ struct alignas(32) GpuNode {
     int32_t pad[4];
 };
 static_assert(sizeof(GpuNode) == 128, "node must be 128 bytes");
+
+// The traversal copy of a GpuNode (ef_scene.cu encode_nodes, after every
+// build / rebuild / refit): each child box as a centre and a half extent
+// per axis, cx[k] +- ex[k] enclosing [lox[k], hix[k]] (e rounded up), so a
+// ray's slab distances are m = c * (1/d) - o/d, near = m - e |1/d|, far =
+// m + e |1/d|: three FMAs per axis, packed two children per FFMA2, and no
+// min/max ordering of the two planes.  Same 128-byte sector
+// layout as GpuNode.  Built with EF_SLAB_CE=0 (A/B) it holds lo / hi.
+#ifndef EF_SLAB_CE
+#define EF_SLAB_CE 1
+#endif
+struct alignas(32) TravNode {
+    float cx[4], ex[4], cy[4], ey[4], cz[4], ez[4];
+    int32_t child[4];
+    int32_t pad[4];
+};
+static_assert(sizeof(TravNode) == 128, "node must be 128 bytes");
 constexpr int32_t kEmptyChild = INT32_MIN;
 
 // f64 triangle payload in BVH leaf order, 96 bytes = three 32-byte sectors
@@ -86,6 +103,8 @@ int device_build_bvh(ef_scene* s, const double* v0, const double* e1, const doub
 // (Re)computes s->shade from s->normals, s->mat and s->pdiff, and s->tri_box
 // from s->tris_by_id and s->pad (ef_scene.cu).
 int update_shade(ef_scene* s, cudaStream_t st);
+// (Re)computes s->tnodes, the traversal form of s->nodes (ef_scene.cu).
+int encode_nodes(ef_scene* s, cudaStream_t st);
 
 }  // namespace ef
 
@@ -99,7 +118,9 @@ struct ef_scene {
     int32_t max_leaf = 0;
     int64_t device_bytes = 0;
     // device buffers
-    ef::GpuNode* nodes = nullptr;      // (n_nodes)
+    ef::GpuNode* nodes = nullptr;      // (n_nodes) build / refit form
+    ef::TravNode* tnodes = nullptr;    // (n_nodes) traversal form (encode_nodes)
+    int64_t n_tnodes_cap = 0;
     ef::GpuTri* tris = nullptr;        // (n_refs) leaf order
     double* tris_by_id = nullptr;      // (n_tri, 9) original order (all-pairs path)
     double* normals = nullptr;         // (n_tri, 3) original order

@@ -28,6 +28,7 @@ cudaError_t upload(T** dst, const T* src, size_t count, int64_t& bytes) {
 void free_scene(ef_scene* s) {
     if (!s) return;
     cudaFree(s->nodes);
+    cudaFree(s->tnodes);
     cudaFree(s->tris);
     cudaFree(s->tris_by_id);
     cudaFree(s->normals);
@@ -105,7 +106,64 @@ __global__ void cluster_kernel(float* clu_box, const int32_t* clu_ids, const flo
     }
 }
 
+// One child box of one axis in the traversal form: centre c (rounded to
+// nearest) and half extent e (rounded up) with [c - e, c + e] enclosing
+// [lo, hi] exactly: hi - c and c - lo are exact in f64 (f32 operands).  An
+// empty slot (lo = hi = +inf) becomes c = +inf, e = 0, which every ray
+// misses: an axis of positive direction gives near = +inf, and a ray with
+// every direction component negative gets far = -inf on every axis.
+__device__ __forceinline__ void encode_slab(float lo, float hi, float& c, float& e) {
+#if EF_SLAB_CE
+    if (isinf(lo) || isinf(hi)) {
+        c = INFINITY;
+        e = 0.0f;
+        return;
+    }
+    c = (float)(0.5 * ((double)lo + (double)hi));
+    e = __double2float_ru(fmax((double)hi - (double)c, (double)c - (double)lo));
+#else
+    c = lo;
+    e = hi;
+#endif
+}
+
+__global__ void encode_nodes_kernel(ef::TravNode* __restrict__ out, const ef::GpuNode* __restrict__ in,
+                                    int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ef::GpuNode g = in[i];
+        ef::TravNode t;
+        for (int k = 0; k < 4; ++k) {
+            encode_slab(g.lox[k], g.hix[k], t.cx[k], t.ex[k]);
+            encode_slab(g.loy[k], g.hiy[k], t.cy[k], t.ey[k]);
+            encode_slab(g.loz[k], g.hiz[k], t.cz[k], t.ez[k]);
+            t.child[k] = g.child[k];
+            t.pad[k] = 0;
+        }
+        out[i] = t;
+    }
+}
+
 }  // namespace
+
+int ef::encode_nodes(ef_scene* s, cudaStream_t st) {
+    if (s->n_nodes == 0) return EF_OK;
+    if (!s->tnodes || s->n_tnodes_cap < s->n_nodes) {
+        if (s->tnodes) {
+            s->device_bytes -= s->n_tnodes_cap * (int64_t)sizeof(TravNode);
+            cudaFree(s->tnodes);
+            s->tnodes = nullptr;
+        }
+        cudaError_t e = cudaMalloc((void**)&s->tnodes, (size_t)s->n_nodes * sizeof(TravNode));
+        if (e != cudaSuccess) return check_cuda(e, "encode_nodes");
+        s->n_tnodes_cap = s->n_nodes;
+        s->device_bytes += s->n_nodes * (int64_t)sizeof(TravNode);
+    }
+    encode_nodes_kernel<<<(int)std::min<int64_t>((s->n_nodes + 255) / 256, 148 * 8), 256, 0, st>>>(
+        s->tnodes, s->nodes, s->n_nodes);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "encode_nodes");
+}
 
 int ef::update_shade(ef_scene* s, cudaStream_t st) {
     if (s->n_tri == 0) return EF_OK;
@@ -303,7 +361,8 @@ extern "C" int ef_scene_create_ex(const double* v0, const double* e1, const doub
             free_scene(s);
             return check_cuda(e, "ef_scene_create upload");
         }
-        const int rc = update_shade(s, nullptr);
+        int rc = encode_nodes(s, nullptr);
+        if (rc == EF_OK) rc = update_shade(s, nullptr);
         if (rc == EF_OK) e = cudaStreamSynchronize(nullptr);
         if (rc != EF_OK || e != cudaSuccess) {
             free_scene(s);
@@ -437,6 +496,7 @@ extern "C" int ef_scene_rebuild(ef_scene* s, const double* v0, const double* e1,
     int rc = check_cuda(cudaGetLastError(), "ef_scene_rebuild");
     s->clu_order.clear();   // the device tree's leaf order from now on
     if (rc == EF_OK) rc = device_build_bvh(s, v0, e1, e2, 3, st);
+    if (rc == EF_OK) rc = encode_nodes(s, st);
     if (rc != EF_OK) return rc;
     return update_shade(s, st);   // after the build: the boxes use its padding
 }
@@ -460,5 +520,6 @@ extern "C" int ef_scene_refit(ef_scene* s, const double* v0, const double* e1, c
             s->nodes, s->tris, s->level_nodes + a, cnt, s->pad);
         count_launch();
     }
-    return check_cuda(cudaGetLastError(), "ef_scene_refit");
+    const int rc2 = check_cuda(cudaGetLastError(), "ef_scene_refit");
+    return rc2 != EF_OK ? rc2 : encode_nodes(s, st);
 }

@@ -13,7 +13,7 @@
 namespace ef {
 
 // ---------------------------------------------------------------------------
-__global__ void intersect_kernel(const GpuNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
+__global__ void intersect_kernel(const TravNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
                                  const double* __restrict__ tris_by_id, int32_t n_tri, bool brute,
                                  const double* __restrict__ o, const double* __restrict__ d,
                                  int64_t n, double t_min, const double* __restrict__ t_max,
@@ -38,7 +38,7 @@ __global__ void intersect_kernel(const GpuNode* __restrict__ nodes, const GpuTri
 // occluded_batch (scene.py:232-252): segment visibility with the
 // reference's limit = dist - RAY_EPS; all-pairs uses t < limit (scene.py:247),
 // the BVH path t <= limit (scene.py:250).
-__global__ void occluded_kernel(const GpuNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
+__global__ void occluded_kernel(const TravNode* __restrict__ nodes, const GpuTri* __restrict__ tris,
                                 const double* __restrict__ tris_by_id, int32_t n_tri, bool brute,
                                 const double* __restrict__ o, const double* __restrict__ tg,
                                 int64_t n, uint8_t* out) {
@@ -155,7 +155,7 @@ extern "C" int ef_intersect_batch(const ef_scene* s, const double* origins, cons
         return set_error(EF_EUNSUPPORTED, "ef_intersect_batch: empty scene is handled by the host");
     }
     const bool brute = mode == 1 || (mode == 0 && s->n_tri <= kBruteMaxTris);
-    intersect_kernel<<<grid_for(n, 128), 128, 0, st>>>(s->nodes, s->tris, s->tris_by_id,
+    intersect_kernel<<<grid_for(n, 128), 128, 0, st>>>(s->tnodes, s->tris, s->tris_by_id,
                                                        (int32_t)s->n_tri, brute, origins, dirs, n,
                                                        t_min, t_max, t_out, tri_out, hit_out);
     count_launch();
@@ -170,7 +170,7 @@ extern "C" int ef_occluded_batch(const ef_scene* s, const double* origins, const
     if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_occluded_batch: empty scene is handled by the host");
     const bool brute = s->n_tri <= kBruteMaxTris;
     occluded_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
-        s->nodes, s->tris, s->tris_by_id, (int32_t)s->n_tri, brute, origins, targets, n, out);
+        s->tnodes, s->tris, s->tris_by_id, (int32_t)s->n_tri, brute, origins, targets, n, out);
     count_launch();
     return check_cuda(cudaGetLastError(), "occluded_kernel");
 }
@@ -275,7 +275,7 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         e = cudaMemsetAsync(scratch, 0, kHdr, st);
         if (e != cudaSuccess) break;
         TraceParams P;
-        P.nodes = s->nodes;
+        P.nodes = s->tnodes;
         P.tris = s->tris;
         P.tris_by_id = s->tris_by_id;
         P.n_tri = (int32_t)s->n_tri;

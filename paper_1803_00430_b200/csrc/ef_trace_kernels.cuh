@@ -118,7 +118,7 @@ __device__ __forceinline__ Hit closest_brute_group(const double* __restrict__ s_
 }
 
 struct TraceParams {
-    const GpuNode* nodes;
+    const TravNode* nodes;   // traversal form (encode_nodes)
     const GpuTri* tris;
     const double* tris_by_id;
     int32_t n_tri;

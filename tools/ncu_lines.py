@@ -1,14 +1,17 @@
 """Aggregate an ncu source page (--print-source cuda,sass CSV) per CUDA line.
 
     ncu -i rep --page source --csv --print-source cuda,sass > src.csv
-    python tools/ncu_lines.py src.csv [top]"""
+    python tools/ncu_lines.py src.csv [top] [--by-ins]
+(--by-ins: lines ordered by executed warp instructions instead of stall samples)"""
 import csv
 import sys
 
 
 def main():
     rows = list(csv.reader(open(sys.argv[1])))
-    top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+    args = [a for a in sys.argv[2:] if not a.startswith("--")]
+    by_ins = "--by-ins" in sys.argv
+    top = int(args[0]) if args else 40
     out = []
     fname = None
     hdr = None
@@ -30,7 +33,7 @@ def main():
         out.append((samples, ins, thr, f"{fname}:{r[0]}", r[1][:90]))
     tot = sum(o[0] for o in out) or 1
     tins = sum(o[1] for o in out) or 1
-    out.sort(reverse=True)
+    out.sort(key=(lambda o: o[1]) if by_ins else (lambda o: o[0]), reverse=True)
     print(f"total stall samples {tot:.0f}, warp instructions {tins:.3g}")
     for s, i, t, loc, src in out[:top]:
         act = t / i if i else 0
