@@ -375,6 +375,22 @@ void build_bvh(const double* v0, const double* e1, const double* e2, int64_t n, 
     int32_t root = B.build(refs, 0);
     if (B.order.size() >= (size_t(1) << 28)) throw std::runtime_error("build_bvh: too many references");
 
+    if (out.keep_binary) {
+        out.binary.resize(B.nodes.size());
+        for (size_t i = 0; i < B.nodes.size(); ++i) {
+            HostBinNode& h = out.binary[i];
+            for (int k = 0; k < 3; ++k) {
+                h.lo[k] = B.nodes[i].box.lo[k];
+                h.hi[k] = B.nodes[i].box.hi[k];
+            }
+            h.left = B.nodes[i].left;
+            h.right = B.nodes[i].right;
+            h.start = B.nodes[i].start;
+            h.count = B.nodes[i].count;
+        }
+        out.binary_root = root;
+    }
+
     // Collapse the binary tree into 4-wide device nodes (repeatedly open the
     // largest inner child until four slots are used), depth-first numbering.
     out.nodes.clear();

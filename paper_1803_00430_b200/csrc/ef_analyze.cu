@@ -470,7 +470,7 @@ static int* analyze_counters(cudaStream_t st, int n, cudaError_t& e) {
 extern "C" int ef_debug_analysis_phases(unsigned long long* out7, int reset) {
     cudaMemcpyFromSymbol(out7, ef::g_phase, sizeof(unsigned long long) * 7);
     if (reset) {
-        unsigned long long z[12] = {0};
+        unsigned long long z[ef::kPhaseSlots] = {0};
         cudaMemcpyToSymbol(ef::g_phase, z, sizeof z);
     }
     return EF_OK;

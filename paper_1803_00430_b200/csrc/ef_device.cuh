@@ -13,12 +13,25 @@ namespace ef {
 #ifdef EF_PROFILE_PHASES
 // debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
 // 2 pops after leaves, 3 shading, 4 segments)
-static __device__ unsigned long long g_phase[12];   // per translation unit
+constexpr int kPhaseSlots = 24;
+#define EF_SPLIT_DEPTH_PROBE 12
+static __device__ unsigned long long g_phase[kPhaseSlots];   // per translation unit
 #define EF_PHASE_T0(v) const long long v = clock64()
 #define EF_PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(clock64() - (v)))
+// traversal-stack counters (tools/probe_simt.py): 12 pushes, 13 pushes past
+// the shared top, 14 pops taken, 15 pops culled by the closest hit, 16-19
+// node visits that hit 0 / 1 / 2 / >= 3 children, 20 leaf visits
+#define EF_STK(i) (++stk[i])
+#define EF_STK_DECL uint32_t stk[9] = {}
+#define EF_STK_FLUSH                                                                  \
+    for (int i_ = 0; i_ < 9; ++i_)                                                    \
+        if (stk[i_]) atomicAdd(&g_phase[12 + i_], (unsigned long long)stk[i_])
 #else
 #define EF_PHASE_T0(v)
 #define EF_PHASE_ADD(i, v)
+#define EF_STK(i)
+#define EF_STK_DECL
+#define EF_STK_FLUSH
 #endif
 
 // ------------------------------------------------ dependent launches ----
@@ -556,6 +569,7 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
     int32_t node = 0;
     bool done = false;
+    EF_STK_DECL;
     for (;;) {
         while (node >= 0) {
             EF_PHASE_T0(tv);
@@ -573,6 +587,17 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
+#ifdef EF_PROFILE_PHASES
+            {
+                const int nh = (k0 != 0xffffffffu) + (k1 != 0xffffffffu) + (k2 != 0xffffffffu) + (k3 != 0xffffffffu);
+                EF_STK(4 + (nh > 3 ? 3 : nh));
+                if (nh > 1) {
+                    stk[0] += nh - 1;
+                    for (int i_ = 0; i_ < nh - 1; ++i_)
+                        if (st.sp + i_ >= EF_SPLIT_DEPTH_PROBE) EF_STK(1);
+                }
+            }
+#endif
             if constexpr (StackT::kPredicated) {
                 st.push_if(pick(ch, k3 & 3u), k3, k3 != 0xffffffffu);
                 st.push_if(pick(ch, k2 & 3u), k2, k2 != 0xffffffffu);
@@ -598,26 +623,40 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                 const uint2 e = st.top();
                 if (__uint_as_float(e.y & ~3u) <= tb) {
                     node = (int32_t)e.x;
+                    EF_STK(2);
                     break;
                 }
+                EF_STK(3);
             }
             EF_PHASE_ADD(0, tv);
             if (done) break;
         }
-        if (done) return h;
+        if (done) {
+            EF_STK_FLUSH;
+            return h;
+        }
         EF_PHASE_T0(tl);
+        EF_STK(8);
         leaf_test(tris, node, ox, oy, oz, dx, dy, dz, t_min, h, tb, n_tris);
         EF_PHASE_ADD(1, tl);
-        if (any_hit && h.id != INT32_MAX) return h;   // shadow rays: any blocker will do
+        if (any_hit && h.id != INT32_MAX) {   // shadow rays: any blocker will do
+            EF_STK_FLUSH;
+            return h;
+        }
         EF_PHASE_T0(tp);
         for (;;) {
-            if (st.sp == 0) return h;
+            if (st.sp == 0) {
+                EF_STK_FLUSH;
+                return h;
+            }
             --st.sp;
             const uint2 e = st.top();
             if (__uint_as_float(e.y & ~3u) <= tb) {
                 node = (int32_t)e.x;
+                EF_STK(2);
                 break;
             }
+            EF_STK(3);
         }
         EF_PHASE_ADD(2, tp);
     }

@@ -75,7 +75,18 @@ struct alignas(16) GpuShade {
 };
 static_assert(sizeof(GpuShade) == 48, "shade record must be 48 bytes");
 
+// The builder's binary tree (kept on request: tools/sim_bottomup.cpp studies
+// other collapse widths with it).
+struct HostBinNode {
+    double lo[3], hi[3];
+    int32_t left, right;     // -1: leaf
+    int64_t start, count;    // leaf: range of `order`
+};
+
 struct HostBvh {
+    bool keep_binary = false;
+    std::vector<HostBinNode> binary;    // keep_binary: the binary tree, root binary_root
+    int32_t binary_root = 0;
     std::vector<GpuNode> nodes;
     std::vector<int32_t> level_nodes;   // node indices grouped by depth (root level first)
     std::vector<int64_t> level_start;   // offsets into level_nodes, size levels + 1

@@ -445,7 +445,7 @@ extern "C" int ef_loudness_batch(const double* avg, int64_t n, int32_t order, co
 #ifdef EF_PROFILE_PHASES
 extern "C" int ef_debug_phases(unsigned long long* out8, int reset) {
     // the phase counters live in each trace translation unit: sum them
-    for (int i = 0; i < 12; ++i) out8[i] = 0;
+    for (int i = 0; i < ef::kPhaseSlots; ++i) out8[i] = 0;
     ef::debug_phases_brute_nb4(out8, reset);
     ef::debug_phases_brute_nb8(out8, reset);
     ef::debug_phases_bvh_nb4(out8, reset);

@@ -11,11 +11,11 @@ cudaError_t trace_dispatch_brute_nb8(int order, const TraceParams& P, cudaStream
 
 #ifdef EF_PROFILE_PHASES
 void debug_phases_brute_nb8(unsigned long long* acc, int reset) {
-    unsigned long long v[12];
+    unsigned long long v[kPhaseSlots];
     cudaMemcpyFromSymbol(v, g_phase, sizeof v);
-    for (int i = 0; i < 12; ++i) acc[i] += v[i];
+    for (int i = 0; i < kPhaseSlots; ++i) acc[i] += v[i];
     if (reset) {
-        unsigned long long z[12] = {0};
+        unsigned long long z[kPhaseSlots] = {0};
         cudaMemcpyToSymbol(g_phase, z, sizeof z);
     }
 }

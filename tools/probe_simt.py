@@ -30,7 +30,7 @@ def main():
     tr.set_sources(w.sources)
     L = _lib.lib()
     L.ef_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    out = np.zeros(12, np.uint64)
+    out = np.zeros(24, np.uint64)
     tr.trace(w.listener, n_rays=n)
     torch.cuda.synchronize()
     L.ef_debug_phases(out.ctypes.data, 1)
@@ -44,6 +44,10 @@ def main():
           f"SIMT efficiency of the node loop {sn / mn:.3f}")
     print(f"  triangle tests {st:.4g} ({st / na:.2f} per segment); 32 x warp max {mt:.4g}: "
           f"efficiency {st / mt:.3f}")
+    k = [float(out[12 + i]) / na for i in range(9)]
+    print(f"  stack per segment: pushes {k[0]:.2f} (past the shared top {k[1]:.3f}), pops taken {k[2]:.2f}, "
+          f"culled {k[3]:.2f}; node visits hitting 0/1/2/3+ children {k[4]:.2f}/{k[5]:.2f}/{k[6]:.2f}/{k[7]:.2f}; "
+          f"leaf visits {k[8]:.2f}")
 
 
 
