@@ -10,6 +10,19 @@
 
 namespace ef {
 
+// A/B build knobs (tools/build_variant.py): nested push branches (default on),
+// early issue of the next node's loads and extra probe loads (experiments,
+// default off)
+#ifndef EF_NESTED_PUSH
+#define EF_NESTED_PUSH 1
+#endif
+#ifndef EF_EARLY_LOAD
+#define EF_EARLY_LOAD 0
+#endif
+#ifndef EF_EXTRA_LOAD
+#define EF_EXTRA_LOAD 0
+#endif
+
 #ifdef EF_PROFILE_PHASES
 // debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
 // 2 pops after leaves, 3 shading, 4 segments)
@@ -432,6 +445,65 @@ __device__ __forceinline__ void node_keys(const RayF& r, const F8& X, const F8& 
 #endif
 }
 
+#if EF_QNODE
+// The ray in the units of the 16-bit plane grid (TravGrid): plane q of an
+// axis is met at t = q * s + b, s = cell / d, b = (lo - o) / d.  A plane's
+// float is built by one PRMT as 2^23 + q (exact), so the FMA below uses
+// B = b - 2^23 s; the cancellation leaves an error below one cell in t
+// (<= 0.5 ulp of 2^23 |s| twice), which the encoder's extra cell on each
+// side of every box covers (ef_scene.cu encode_planes).  sel: PRMT selector
+// of the near plane's half word (lo for a positive direction).
+struct RayQ {
+    float sx, sy, sz;
+    float Bx, By, Bz;
+    uint32_t selx, sely, selz;
+};
+
+__device__ __forceinline__ RayQ make_rayq(const RayF& r, const F8& G) {
+    RayQ q;
+    q.sx = __fmul_rn(G.e, r.ix);
+    q.sy = __fmul_rn(G.f, r.iy);
+    q.sz = __fmul_rn(G.g, r.iz);
+    q.Bx = __fmaf_rn(-8388608.0f, q.sx, __fmaf_rn(G.a, r.ix, -r.ox));
+    q.By = __fmaf_rn(-8388608.0f, q.sy, __fmaf_rn(G.b, r.iy, -r.oy));
+    q.Bz = __fmaf_rn(-8388608.0f, q.sz, __fmaf_rn(G.c, r.iz, -r.oz));
+    q.selx = r.ix >= 0.0f ? 0x7410u : 0x7432u;
+    q.sely = r.iy >= 0.0f ? 0x7410u : 0x7432u;
+    q.selz = r.iz >= 0.0f ? 0x7410u : 0x7432u;
+    return q;
+}
+
+// near / far parameters of one axis for the four children (words w0..w3)
+__device__ __forceinline__ void slab_q4(float w0, float w1, float w2, float w3, uint32_t sel, float s, float B,
+                                        float* tn, float* tf) {
+    const uint32_t self = sel ^ 0x0022u;   // the other half word
+    const uint32_t u0 = __float_as_uint(w0), u1 = __float_as_uint(w1), u2 = __float_as_uint(w2),
+                   u3 = __float_as_uint(w3);
+    const f32x2_t ss = pack2(s, s), bb = pack2(B, B);
+    unpack2(ffma2(pack2(__uint_as_float(__byte_perm(u0, 0x4B000000u, sel)),
+                        __uint_as_float(__byte_perm(u1, 0x4B000000u, sel))), ss, bb), tn[0], tn[1]);
+    unpack2(ffma2(pack2(__uint_as_float(__byte_perm(u2, 0x4B000000u, sel)),
+                        __uint_as_float(__byte_perm(u3, 0x4B000000u, sel))), ss, bb), tn[2], tn[3]);
+    unpack2(ffma2(pack2(__uint_as_float(__byte_perm(u0, 0x4B000000u, self)),
+                        __uint_as_float(__byte_perm(u1, 0x4B000000u, self))), ss, bb), tf[0], tf[1]);
+    unpack2(ffma2(pack2(__uint_as_float(__byte_perm(u2, 0x4B000000u, self)),
+                        __uint_as_float(__byte_perm(u3, 0x4B000000u, self))), ss, bb), tf[2], tf[3]);
+}
+
+// A = px[0..3] py[0..3], Bz = pz[0..3] (the node's second sector also holds the children)
+__device__ __forceinline__ void node_keys_q(const RayQ& r, const F8& A, const F8& Bz, float tmin, float tmax,
+                                            uint32_t& k0, uint32_t& k1, uint32_t& k2, uint32_t& k3) {
+    float nx[4], fx[4], ny[4], fy[4], nz[4], fz[4];
+    slab_q4(A.a, A.b, A.c, A.d, r.selx, r.sx, r.Bx, nx, fx);
+    slab_q4(A.e, A.f, A.g, A.h, r.sely, r.sy, r.By, ny, fy);
+    slab_q4(Bz.a, Bz.b, Bz.c, Bz.d, r.selz, r.sz, r.Bz, nz, fz);
+    k0 = slab_key_ce(nx[0], fx[0], ny[0], fy[0], nz[0], fz[0], tmin, tmax, 0u);
+    k1 = slab_key_ce(nx[1], fx[1], ny[1], fy[1], nz[1], fz[1], tmin, tmax, 1u);
+    k2 = slab_key_ce(nx[2], fx[2], ny[2], fy[2], nz[2], fz[2], tmin, tmax, 2u);
+    k3 = slab_key_ce(nx[3], fx[3], ny[3], fy[3], nz[3], fz[3], tmin, tmax, 3u);
+}
+#endif
+
 __device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
     a = lo;
@@ -565,11 +637,18 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                                            StackT& st, bool any_hit = false) {
     Hit h{t_max, INT32_MAX};
     const RayF r = make_rayf(ox, oy, oz, dx, dy, dz);
+#if EF_QNODE
+    const RayQ rq = make_rayq(r, ldg_f8(nodes - 1));   // the slot before node 0 holds the grid
+#endif
     const float tminf = fmaxf(__double2float_rd(t_min), 0.0f);
     float tb = fminf(__double2float_ru(t_max), 1e38f);   // finite: empty slots must miss
     int32_t node = 0;
     bool done = false;
     EF_STK_DECL;
+#if EF_EARLY_LOAD
+    F8 X = ldg_f8(nodes->cx), Y = ldg_f8(nodes->cy), Z = ldg_f8(nodes->cz);
+    int4 chn = __ldg(reinterpret_cast<const int4*>(nodes->child));
+#endif
     for (;;) {
         while (node >= 0) {
             EF_PHASE_T0(tv);
@@ -577,16 +656,57 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             ++n_nodes;
 #endif
             // three 256-bit loads (lo/hi planes of x, y, z), one 128-bit (children)
+#if EF_QNODE
+            // two 256-bit loads: x and y plane words, z plane words + children
+            const TravNode* q = nodes + node;
+            const F8 X = ldg_f8(q->px), Z = ldg_f8(q->pz);
+            const int4 ch = make_int4(__float_as_int(Z.e), __float_as_int(Z.f), __float_as_int(Z.g),
+                                      __float_as_int(Z.h));
+#elif EF_EARLY_LOAD
+            const int4 ch = chn;
+#else
             const TravNode* q = nodes + node;
             const F8 X = ldg_f8(q->cx), Y = ldg_f8(q->cy), Z = ldg_f8(q->cz);
             const int4 ch = __ldg(reinterpret_cast<const int4*>(q->child));
+#if EF_EXTRA_LOAD   // sensitivity probe: one more 16-byte load per node visit (same sector as the children)
+            {
+                int4 junk;
+                asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(junk.x), "=r"(junk.y), "=r"(junk.z), "=r"(junk.w) : "l"(q->pad));
+#if EF_EXTRA_LOAD > 1   // ... and a 32-byte load of another line (the next node's first sector)
+                F8 j2;
+                asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                    : "=f"(j2.a), "=f"(j2.b), "=f"(j2.c), "=f"(j2.d), "=f"(j2.e), "=f"(j2.f), "=f"(j2.g), "=f"(j2.h)
+                    : "l"((q + 1)->cx));
+                n_nodes += (j2.a == 1.2345e-30f) + (j2.h == 1.2345e-30f);
+#endif
+                n_nodes += (junk.x == 0x12345678) + (junk.w == 0x12345678);   // never true: keeps the loads
+            }
+#endif
+#endif
             uint32_t k0, k1, k2, k3;
+#if EF_QNODE
+            node_keys_q(rq, X, Z, tminf, tb, k0, k1, k2, k3);
+#else
             node_keys(r, X, Y, Z, tminf, tb, k0, k1, k2, k3);
+#endif
             kswap(k0, k1);
             kswap(k2, k3);
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
+#if EF_EARLY_LOAD
+            // the nearest child's node is fetched before the farther hits are
+            // pushed: the push code runs under the loads' latency (a leaf or
+            // a miss fetches the root: harmless, no branch)
+            const int32_t next = k0 != 0xffffffffu ? pick(ch, k0 & 3u) : -1;
+            {
+                const TravNode* q = nodes + max(next, 0);
+                X = ldg_f8(q->cx);
+                Y = ldg_f8(q->cy);
+                Z = ldg_f8(q->cz);
+                chn = __ldg(reinterpret_cast<const int4*>(q->child));
+            }
+#endif
 #ifdef EF_PROFILE_PHASES
             {
                 const int nh = (k0 != 0xffffffffu) + (k1 != 0xffffffffu) + (k2 != 0xffffffffu) + (k3 != 0xffffffffu);
@@ -603,12 +723,29 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                 st.push_if(pick(ch, k2 & 3u), k2, k2 != 0xffffffffu);
                 st.push_if(pick(ch, k1 & 3u), k1, k1 != 0xffffffffu);
             } else {
+#if EF_NESTED_PUSH
+                // keys are sorted and a miss is the largest key: k1 missing
+                // means k2 and k3 are missing too (76% of C5's node visits
+                // hit one child: one not-taken branch instead of three)
+                if (k1 != 0xffffffffu) {
+                    if (k2 != 0xffffffffu) {
+                        if (k3 != 0xffffffffu) st.push(pick(ch, k3 & 3u), k3);
+                        st.push(pick(ch, k2 & 3u), k2);
+                    }
+                    st.push(pick(ch, k1 & 3u), k1);
+                }
+#else
                 if (k3 != 0xffffffffu) st.push(pick(ch, k3 & 3u), k3);
                 if (k2 != 0xffffffffu) st.push(pick(ch, k2 & 3u), k2);
                 if (k1 != 0xffffffffu) st.push(pick(ch, k1 & 3u), k1);
+#endif
             }
             if (k0 != 0xffffffffu) {
+#if EF_EARLY_LOAD
+                node = next;
+#else
                 node = pick(ch, k0 & 3u);
+#endif
                 EF_PHASE_ADD(0, tv);
                 continue;
             }
@@ -630,6 +767,15 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             }
             EF_PHASE_ADD(0, tv);
             if (done) break;
+#if EF_EARLY_LOAD
+            if (node >= 0) {
+                const TravNode* q = nodes + node;
+                X = ldg_f8(q->cx);
+                Y = ldg_f8(q->cy);
+                Z = ldg_f8(q->cz);
+                chn = __ldg(reinterpret_cast<const int4*>(q->child));
+            }
+#endif
         }
         if (done) {
             EF_STK_FLUSH;
@@ -659,6 +805,15 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             EF_STK(3);
         }
         EF_PHASE_ADD(2, tp);
+#if EF_EARLY_LOAD
+        if (node >= 0) {
+            const TravNode* q = nodes + node;
+            X = ldg_f8(q->cx);
+            Y = ldg_f8(q->cy);
+            Z = ldg_f8(q->cz);
+            chn = __ldg(reinterpret_cast<const int4*>(q->child));
+        }
+#endif
     }
 }
 

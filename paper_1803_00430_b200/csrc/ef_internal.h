@@ -45,12 +45,40 @@ static_assert(sizeof(GpuNode) == 128, "node must be 128 bytes");
 #ifndef EF_SLAB_CE
 #define EF_SLAB_CE 1
 #endif
+// EF_QNODE = 1 (default): the traversal copy is 64 bytes, two 256-bit loads
+// per node visit instead of four loads.  Every plane of the four child
+// boxes is a 16-bit coordinate on a grid over the scene's bounds (TravGrid,
+// stored in the slot before node 0): word k of an axis = lo | hi << 16 of
+// child k, lo rounded down and hi up to the grid and each widened by one
+// more cell, which covers the rounding of the ray-space evaluation (one
+// PRMT per plane builds the float 2^23 + q, one FMA maps it to the ray
+// parameter).  An empty slot is lo = 65535, hi = 0 on every
+// axis (near > far for every direction).
+#ifndef EF_QNODE
+#define EF_QNODE 1
+#endif
+#if EF_QNODE
+struct alignas(32) TravNode {
+    uint32_t px[4], py[4], pz[4];
+    int32_t child[4];
+};
+static_assert(sizeof(TravNode) == 64, "node must be 64 bytes");
+// the grid: plane q of axis a lies at lo[a] + q * cell[a]
+struct alignas(32) TravGrid {
+    float lo[3], pad0;
+    float cell[3], pad1;
+    float fill[8];
+};
+static_assert(sizeof(TravGrid) == sizeof(TravNode), "the grid takes one node slot");
+constexpr uint32_t kEmptyPlanes = 0x0000ffffu;
+#else
 struct alignas(32) TravNode {
     float cx[4], ex[4], cy[4], ey[4], cz[4], ez[4];
     int32_t child[4];
     int32_t pad[4];
 };
 static_assert(sizeof(TravNode) == 128, "node must be 128 bytes");
+#endif
 constexpr int32_t kEmptyChild = INT32_MIN;
 
 // f64 triangle payload in BVH leaf order, 96 bytes = three 32-byte sectors
@@ -130,7 +158,9 @@ struct ef_scene {
     int64_t device_bytes = 0;
     // device buffers
     ef::GpuNode* nodes = nullptr;      // (n_nodes) build / refit form
-    ef::TravNode* tnodes = nullptr;    // (n_nodes) traversal form (encode_nodes)
+    ef::TravNode* tnodes = nullptr;    // (n_nodes) traversal form (encode_nodes); EF_QNODE: tnodes[-1]
+                                       // holds the TravGrid (tnodes_base is the allocation)
+    ef::TravNode* tnodes_base = nullptr;
     int64_t n_tnodes_cap = 0;
     ef::GpuTri* tris = nullptr;        // (n_refs) leaf order
     double* tris_by_id = nullptr;      // (n_tri, 9) original order (all-pairs path)

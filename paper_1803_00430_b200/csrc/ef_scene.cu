@@ -28,7 +28,7 @@ cudaError_t upload(T** dst, const T* src, size_t count, int64_t& bytes) {
 void free_scene(ef_scene* s) {
     if (!s) return;
     cudaFree(s->nodes);
-    cudaFree(s->tnodes);
+    cudaFree(s->tnodes_base);
     cudaFree(s->tris);
     cudaFree(s->tris_by_id);
     cudaFree(s->normals);
@@ -106,6 +106,7 @@ __global__ void cluster_kernel(float* clu_box, const int32_t* clu_ids, const flo
     }
 }
 
+#if !EF_QNODE
 // One child box of one axis in the traversal form: centre c (rounded to
 // nearest) and half extent e (rounded up) with [c - e, c + e] enclosing
 // [lo, hi] exactly: hi - c and c - lo are exact in f64 (f32 operands).  An
@@ -126,7 +127,62 @@ __device__ __forceinline__ void encode_slab(float lo, float hi, float& c, float&
     e = hi;
 #endif
 }
+#endif
 
+#if EF_QNODE
+// The 16-bit grid over the root's child boxes (the scene's padded bounds),
+// three cells of margin on each side so the widened planes stay in range.
+__global__ void encode_grid_kernel(ef::TravGrid* __restrict__ grid, const ef::GpuNode* __restrict__ in) {
+    const ef::GpuNode g = in[0];
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = 0; k < 4; ++k) {
+        if (g.child[k] == ef::kEmptyChild) continue;
+        lo[0] = fminf(lo[0], g.lox[k]); hi[0] = fmaxf(hi[0], g.hix[k]);
+        lo[1] = fminf(lo[1], g.loy[k]); hi[1] = fmaxf(hi[1], g.hiy[k]);
+        lo[2] = fminf(lo[2], g.loz[k]); hi[2] = fmaxf(hi[2], g.hiz[k]);
+    }
+    ef::TravGrid t = {};
+    float scale = 1e-30f;
+    for (int a = 0; a < 3; ++a) scale = fmaxf(scale, fmaxf(fabsf(lo[a]), fabsf(hi[a])));
+    for (int a = 0; a < 3; ++a) {
+        // a flat axis still gets cells of finite size
+        const double ext = fmax((double)hi[a] - (double)lo[a], 1e-6 * (double)scale);
+        const float cell = __double2float_ru(ext / 65528.0);
+        t.cell[a] = cell;
+        t.lo[a] = __double2float_rd((double)lo[a] - 3.0 * (double)cell);
+    }
+    *grid = t;
+}
+
+// lo | hi << 16 of one child box on one axis: floor / ceil to the grid and
+// one more cell outward (the traversal's arithmetic error is below one
+// cell, ef_device.cuh slab_q2)
+__device__ __forceinline__ uint32_t encode_planes(float lo, float hi, float glo, float cell) {
+    if (isinf(lo) || isinf(hi)) return ef::kEmptyPlanes;
+    const double ql = floor(((double)lo - (double)glo) / (double)cell) - 1.0;
+    const double qh = ceil(((double)hi - (double)glo) / (double)cell) + 1.0;
+    const uint32_t l = (uint32_t)fmin(fmax(ql, 0.0), 65535.0), h = (uint32_t)fmin(fmax(qh, 0.0), 65535.0);
+    return l | (h << 16);
+}
+
+__global__ void encode_nodes_kernel(ef::TravNode* __restrict__ out, const ef::GpuNode* __restrict__ in,
+                                    int64_t n) {
+    const ef::TravGrid G = *reinterpret_cast<const ef::TravGrid*>(out - 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const ef::GpuNode g = in[i];
+        ef::TravNode t;
+        for (int k = 0; k < 4; ++k) {
+            const bool empty = g.child[k] == ef::kEmptyChild;
+            t.px[k] = empty ? ef::kEmptyPlanes : encode_planes(g.lox[k], g.hix[k], G.lo[0], G.cell[0]);
+            t.py[k] = empty ? ef::kEmptyPlanes : encode_planes(g.loy[k], g.hiy[k], G.lo[1], G.cell[1]);
+            t.pz[k] = empty ? ef::kEmptyPlanes : encode_planes(g.loz[k], g.hiz[k], G.lo[2], G.cell[2]);
+            t.child[k] = g.child[k];
+        }
+        out[i] = t;
+    }
+}
+#else
 __global__ void encode_nodes_kernel(ef::TravNode* __restrict__ out, const ef::GpuNode* __restrict__ in,
                                     int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -143,22 +199,29 @@ __global__ void encode_nodes_kernel(ef::TravNode* __restrict__ out, const ef::Gp
         out[i] = t;
     }
 }
+#endif
 
 }  // namespace
 
+// The allocation has one slot before node 0 (EF_QNODE: the TravGrid).
 int ef::encode_nodes(ef_scene* s, cudaStream_t st) {
     if (s->n_nodes == 0) return EF_OK;
     if (!s->tnodes || s->n_tnodes_cap < s->n_nodes) {
-        if (s->tnodes) {
-            s->device_bytes -= s->n_tnodes_cap * (int64_t)sizeof(TravNode);
-            cudaFree(s->tnodes);
-            s->tnodes = nullptr;
+        if (s->tnodes_base) {
+            s->device_bytes -= (s->n_tnodes_cap + 1) * (int64_t)sizeof(TravNode);
+            cudaFree(s->tnodes_base);
+            s->tnodes_base = s->tnodes = nullptr;
         }
-        cudaError_t e = cudaMalloc((void**)&s->tnodes, (size_t)s->n_nodes * sizeof(TravNode));
+        cudaError_t e = cudaMalloc((void**)&s->tnodes_base, (size_t)(s->n_nodes + 1) * sizeof(TravNode));
         if (e != cudaSuccess) return check_cuda(e, "encode_nodes");
+        s->tnodes = s->tnodes_base + 1;
         s->n_tnodes_cap = s->n_nodes;
-        s->device_bytes += s->n_nodes * (int64_t)sizeof(TravNode);
+        s->device_bytes += (s->n_nodes + 1) * (int64_t)sizeof(TravNode);
     }
+#if EF_QNODE
+    encode_grid_kernel<<<1, 1, 0, st>>>(reinterpret_cast<TravGrid*>(s->tnodes_base), s->nodes);
+    count_launch();
+#endif
     encode_nodes_kernel<<<(int)std::min<int64_t>((s->n_nodes + 255) / 256, 148 * 8), 256, 0, st>>>(
         s->tnodes, s->nodes, s->n_nodes);
     count_launch();

@@ -24,21 +24,32 @@
 
 namespace ef {
 
-// One fat CTA per SM: 512 threads, 128 registers.  (Scenes whose nodes +
-// triangles exceed kBigSceneBytes -- L1 cannot hold them: C3, C5 -- ran 768
-// threads at 80 registers in round 1; with the compile-time stack shapes the
-// 512-thread kernel is faster there too: C5 3.84 vs 3.62 (768) / 3.71 (640)
-// / 3.32 (384) G seg/s, C3 2.39 vs 2.38 / 2.42 / 2.05, r02f.)  Big scenes
-// keep the split stack (shared top + local overflow) since their trees'
-// whole stack does not fit in shared memory.
-constexpr int kSmallThreads = 512;
+// One fat CTA per SM.  Scenes whose whole traversal stack fits in shared
+// memory (C2) and the all-pairs scenes (C1) run 512 threads at 128
+// registers.  Every other scene (C3, C5: nodes + triangles far beyond L1)
+// runs kBigThreads = 1024 threads at 64 registers with the split stack
+// (shared top + local overflow): with the 64-byte quantized nodes a node
+// visit holds 16 node registers instead of 28, the spills that remain sit
+// in the per-segment code, and twice the warps hide the dependent L1/L2
+// latency of the descent (C5 4.02 -> 4.23, C3 2.69 -> 3.08 G seg/s against
+// 512 threads; 768: 4.03 / 2.85, 896: 4.21 / 3.06; C2 loses at more than
+// 512: 1.73 -> 1.46).  Tuning builds: EF_TRACE_THREADS, EF_BIG_THREADS.
+#ifndef EF_TRACE_THREADS
+#define EF_TRACE_THREADS 512
+#endif
+#ifndef EF_BIG_THREADS
+#define EF_BIG_THREADS 1024
+#endif
+constexpr int kSmallThreads = EF_TRACE_THREADS;
+constexpr int kBigThreads = EF_BIG_THREADS;
 constexpr int64_t kBigSceneBytes = 4ll << 20;
 // Shared traversal-stack entries per thread (the rest in local memory) when
-// the tree's whole stack does not fit: 12 x 512 threads (48 KB), columns for
-// THREADS threads (compile-time stride).  (8 / 12 / 16 entries: C5 3.867 /
-// 3.862 / 3.839, C3 2.384 / 2.398 / 2.389 G seg/s, r02i -- flat.)
+// the tree's whole stack does not fit: 6 x 1024 threads (48 KB; 4 / 8 / 12
+// entries: C5 4.21 / 4.23 / 4.19 against 4.25, C3 within 1%), columns for
+// THREADS threads (compile-time stride).  A C5 segment pushes 2.8 entries
+// and its stack never passes 12 (tools/probe_simt.py).
 #ifndef EF_SPLIT_DEPTH
-#define EF_SPLIT_DEPTH 12
+#define EF_SPLIT_DEPTH 6
 #endif
 template <int THREADS>
 constexpr int kSplitDepth = EF_SPLIT_DEPTH;
@@ -1021,9 +1032,9 @@ static cudaError_t dispatch_brute(int order, const TraceParams& P, cudaStream_t 
 
 template <int NBMAX>
 static cudaError_t dispatch_bvh(bool big, int order, const TraceParams& P, cudaStream_t st) {
+    (void)big;
     if (P.smem_stack > 0) return dispatch_order<NBMAX, false, kSmallThreads, 1, true>(order, P, st);
-    if (big) return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
-    return dispatch_order<NBMAX, false, kSmallThreads>(order, P, st);
+    return dispatch_order<NBMAX, false, kBigThreads>(order, P, st);
 }
 
 // Defined one per translation unit (ef_trace_{brute,bvh}_nb{4,8}.cu).

@@ -48,6 +48,102 @@ static double harea(const HostBinNode& n) {
     return dx * dy + dy * dz + dz * dx;
 }
 
+// SAH-optimal collapse (dynamic programme of Ylitie, Karras & Laine 2017,
+// section 3.1, with the builder's leaves kept): cost[n][i] = least sum of
+// wide-node areas for the subtree of binary node n represented by at most
+// i + 1 roots; a wide node's W children are the best W-root forest.
+static void collapse_dp(Tree& T, int W) {
+    const auto& B = T.b.binary;
+    const size_t nb = B.size();
+    std::vector<double> cost(nb * W, 0.0);       // [n][i], i = 0..W-1 -> at most i+1 roots
+    std::vector<int8_t> split(nb * W, 0);        // k (roots given to the left child), 0: use [i-1]
+    std::vector<double> dist(nb * (W + 1), 0.0); // distribute cost for j = 2..W roots
+    std::vector<int8_t> dsplit(nb * (W + 1), 0);
+    // post-order over the binary tree
+    std::vector<int32_t> order, st = {T.b.binary_root};
+    while (!st.empty()) {
+        const int32_t n = st.back();
+        st.pop_back();
+        order.push_back(n);
+        if (B[n].left >= 0) { st.push_back(B[n].left); st.push_back(B[n].right); }
+    }
+    for (size_t q = order.size(); q-- > 0;) {
+        const int32_t n = order[q];
+        if (B[n].left < 0) {
+            for (int i = 0; i < W; ++i) cost[n * W + i] = 0.0;   // leaves cost the same in every collapse
+            continue;
+        }
+        const int32_t l = B[n].left, r = B[n].right;
+        for (int j = 2; j <= W; ++j) {
+            double best = INFINITY;
+            int bk = 1;
+            for (int k = 1; k < j; ++k) {
+                const double c = cost[l * W + (k - 1)] + cost[r * W + (j - k - 1)];
+                if (c < best) { best = c; bk = k; }
+            }
+            dist[n * (W + 1) + j] = best;
+            dsplit[n * (W + 1) + j] = (int8_t)bk;
+        }
+        cost[n * W + 0] = dist[n * (W + 1) + W] + harea(B[n]);   // one root: n is a wide node
+        for (int i = 1; i < W; ++i) {
+            const double d = dist[n * (W + 1) + (i + 1)];
+            if (d < cost[n * W + i - 1]) { cost[n * W + i] = d; split[n * W + i] = 1; }
+            else { cost[n * W + i] = cost[n * W + i - 1]; split[n * W + i] = 0; }
+        }
+    }
+    // roots of the best (<= i+1)-root forest of subtree n
+    struct F { int32_t n; int i; };
+    auto forest = [&](int32_t n0, int j0, std::vector<int32_t>& out) {
+        // distribute j0 roots over n0's children
+        std::vector<F> fs;
+        const int k0 = dsplit[n0 * (W + 1) + j0];
+        fs.push_back({B[n0].left, k0 - 1});
+        fs.push_back({B[n0].right, j0 - k0 - 1});
+        while (!fs.empty()) {
+            F f = fs.back();
+            fs.pop_back();
+            if (B[f.n].left < 0) { out.push_back(f.n); continue; }
+            int i = f.i;
+            while (i > 0 && split[f.n * W + i] == 0) --i;
+            if (i == 0) { out.push_back(f.n); continue; }   // a single root: wide node (or leaf)
+            const int j = i + 1, k = dsplit[f.n * (W + 1) + j];
+            fs.push_back({B[f.n].left, k - 1});
+            fs.push_back({B[f.n].right, j - k - 1});
+        }
+    };
+    struct Item { int32_t bn; int32_t slot; int depth; };
+    std::vector<Item> stack;
+    T.nodes.push_back({0, 0});
+    stack.push_back({T.b.binary_root, 0, 1});
+    const float pad = (float)T.b.pad;
+    while (!stack.empty()) {
+        Item it = stack.back();
+        stack.pop_back();
+        T.depth = std::max(T.depth, it.depth);
+        std::vector<int32_t> kids;
+        forest(it.bn, W, kids);
+        WNode nd{(int)T.kids.size(), (int)kids.size()};
+        const size_t base = T.kids.size();
+        T.kids.resize(base + kids.size());
+        for (size_t c = 0; c < kids.size(); ++c) {
+            const HostBinNode& ch = B[kids[c]];
+            WChild k;
+            for (int a = 0; a < 3; ++a) {
+                k.lo[a] = std::nextafterf((float)(ch.lo[a] - pad), -INFINITY);
+                k.hi[a] = std::nextafterf((float)(ch.hi[a] + pad), INFINITY);
+            }
+            if (ch.left < 0) k.ref = ~(int32_t)((ch.start << 3) | (ch.count - 1));
+            else {
+                k.ref = (int32_t)T.nodes.size();
+                T.nodes.push_back({0, 0});
+                stack.push_back({kids[c], k.ref, it.depth + 1});
+            }
+            T.kids[base + c] = k;
+        }
+        T.nodes[it.slot] = nd;
+    }
+}
+
 static void collapse(Tree& T, int W) {
     const auto& B = T.b.binary;
     struct Item { int32_t bn; int32_t slot; int depth; };
@@ -168,7 +264,8 @@ int main(int argc, char** argv) {
     Tree T;
     T.b.keep_binary = true;
     build_bvh(v0.data(), e1.data(), e2.data(), n, T.b);
-    collapse(T, W);
+    if (argc > 6 && std::atoi(argv[6]) == 1) collapse_dp(T, W);
+    else collapse(T, W);
     const size_t nr = T.b.order.size();
     T.tri.resize(9 * nr);
     for (size_t i = 0; i < nr; ++i) {
