@@ -466,11 +466,15 @@ def run_gpu(args, w, metric, unit):
     # DRAM bytes of the trace call from the committed ncu captures: the trace
     # kernel plus, where the scene has one, the frame's tail kernel
     traffic = None
+    ncu_util = None
     for suffix in ("", "tail"):
         tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}{suffix}.json")
         if os.path.exists(tf):
             with open(tf) as f:
-                traffic = (traffic or 0.0) + json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            traffic = (traffic or 0.0) + tj.get("dram_bytes_per_launch")
+            if not suffix:
+                ncu_util = tj.get("utilisation")
     if world > 1:
         if fused:
             peers.close()
@@ -481,12 +485,14 @@ def run_gpu(args, w, metric, unit):
     if rank != 0:
         return
     # device-work roofline: the bytes the device kernels themselves touch per
-    # segment (their own counters: 128-byte 4-wide nodes visited, 80-byte
-    # triangle records tested, one 48-byte shading record + two f32 factor
-    # rows per segment, a histogram read-modify-write per arrival), against
-    # the measured L2 bandwidth (tools/micro/cache_bw.cu,
-    # profiles/micro_peaks.json): the working set is L1/L2-resident
-    dev_bytes = (128.0 * nodes_step + 80.0 * tris_step + (48 + 8 * sc.n_bands) * segs_per_step
+    # segment (their own counters: 64-byte quantized 4-wide nodes visited,
+    # 80 bytes of each triangle record tested, one 48-byte shading record +
+    # two f32 factor rows per segment, a histogram read-modify-write per
+    # arrival), against the measured L2 bandwidth (tools/micro/cache_bw.cu,
+    # profiles/micro_peaks.json): the working set is L1/L2-resident.  What
+    # binds the kernel is in "ncu": issue-slot, ALU-pipe and L1/TEX
+    # utilisation of the committed capture (profiles/traffic_<config>.json)
+    dev_bytes = (64.0 * nodes_step + 80.0 * tris_step + (48 + 8 * sc.n_bands) * segs_per_step
                  + arr_step * 8 * sc.n_bands * nk)
     micro = {}
     mp = os.path.join(ROOT, "profiles", "micro_peaks.json")
@@ -500,7 +506,8 @@ def run_gpu(args, w, metric, unit):
                 "bytes_per_segment": dev_bytes / max(segs_per_step, 1.0),
                 "nodes_per_segment": nodes_step / max(segs_per_step, 1.0),
                 "triangles_per_segment": tris_step / max(segs_per_step, 1.0),
-                "peak_source": "profiles/micro_peaks.json (tools/micro/cache_bw.cu)" if micro else None}
+                "peak_source": "profiles/micro_peaks.json (tools/micro/cache_bw.cu)" if micro else None,
+                "ncu": ncu_util}
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

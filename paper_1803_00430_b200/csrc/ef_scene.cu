@@ -55,7 +55,7 @@ __global__ void shade_kernel(GpuShade* out, const double* normals, const int32_t
         for (int k = 0; k < 3; ++k) r.n[k] = normals[3 * i + k];
         r.m = mat[i];
         r.p = pdiff[r.m];
-        r.pad[0] = r.pad[1] = r.pad[2] = 0;
+        for (int k = 0; k < (int)(sizeof(r.pad) / sizeof(r.pad[0])); ++k) r.pad[k] = 0;
         out[i] = r;
     }
 }

@@ -370,14 +370,17 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
         const bool sstack_fits = max_stack <= kStackSize && sstack_bytes <= sstack_max;
         P.smem_stack = (!brute && (!big || sstack_max != kMaxSstackBytes) && sstack_env && sstack_fits)
                            ? max_stack : 0;
+        // the tail hand-off is compiled into the shared-stack kernel only
+        // (scenes of <= kTailMaxTris triangles whose whole stack fits)
+        if (P.smem_stack == 0) P.tail_live = 0;
         if (s->n_bands <= 4) {
             e = brute ? trace_dispatch_brute_nb4(cfg->order, P, st)
                       : trace_dispatch_bvh_nb4(big, cfg->order, P, st);
-            if (e == cudaSuccess && tail_live > 0) e = tail_dispatch_nb4(cfg->order, P, st);
+            if (e == cudaSuccess && P.tail_live > 0) e = tail_dispatch_nb4(cfg->order, P, st);
         } else {
             e = brute ? trace_dispatch_brute_nb8(cfg->order, P, st)
                       : trace_dispatch_bvh_nb8(big, cfg->order, P, st);
-            if (e == cudaSuccess && tail_live > 0) e = tail_dispatch_nb8(cfg->order, P, st);
+            if (e == cudaSuccess && P.tail_live > 0) e = tail_dispatch_nb8(cfg->order, P, st);
         }
         if (e != cudaSuccess) break;
     }

@@ -441,10 +441,18 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         if (S.nrefl == 2) S.tri1 = h.id;
         ls.c[EF_ST_REFLECTIONS]++;
         // one 48-byte shading record, one level of loads: normal, p_m, material
+#if EF_SHADE64
+        const GpuShade* rec = P.shade + h.id;
+        D4 r01;
+        asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r01.x), "=d"(r01.y), "=d"(r01.z), "=d"(r01.w) : "l"(rec));
+        const int m = __ldg(&rec->m);
+        const double nx = r01.x, ny = r01.y, nz = r01.z, pdiff = r01.w;
+#else
         const double2* rec = reinterpret_cast<const double2*>(P.shade + h.id);
         const double2 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1);
         const int m = __ldg(reinterpret_cast<const int*>(rec + 2));
         const double nx = r0.x, ny = r0.y, nz = r1.x, pdiff = r1.y;
+#endif
         double u1, u2;
         uint4 xg;   // lane groups: this lane's draw (ray, bounce, gl) -- all of a
                     // group's draws come from one Philox latency instead of a chain
@@ -506,9 +514,20 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         }
         S.last_diffuse = diffuse;
         const float* f = (diffuse ? P.fd : P.fs) + m * nb;
+        // one vector load per row when it is a whole aligned row (nb = 4 or
+        // 8: the tables are cudaMalloc'ed, rows nb floats apart)
+        if (NBMAX == 8 && nb == 8) {
+            const F8 r = ldg_f8(f);
+            S.E[0] *= r.a; S.E[1] *= r.b; S.E[2] *= r.c; S.E[3] *= r.d;
+            if constexpr (NBMAX == 8) { S.E[4] *= r.e; S.E[5] *= r.f; S.E[6] *= r.g; S.E[7] *= r.h; }
+        } else if (nb == 4) {
+            const float4 r = __ldg(reinterpret_cast<const float4*>(f));
+            S.E[0] *= r.x; S.E[1] *= r.y; S.E[2] *= r.z; S.E[3] *= r.w;
+        } else {
 #pragma unroll
-        for (int b = 0; b < NBMAX; ++b)
-            if (b < nb) S.E[b] = S.E[b] * __ldg(f + b);
+            for (int b = 0; b < NBMAX; ++b)
+                if (b < nb) S.E[b] = S.E[b] * __ldg(f + b);
+        }
         if (diffuse) {
             const double s = nd > 0.0 ? -1.0 : 1.0;
             // basis of the normal facing the incoming side (a precomputed
@@ -626,7 +645,7 @@ __global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) 
         // the path counter is exhausted and at most tail_live paths are
         // unfinished, the warp's live paths move to the continuation list
         // for tail_kernel, which runs each on a whole CTA
-        if (P.tail_live > 0) {
+        if (SSTACK && P.tail_live > 0) {   // (ef_trace.cu: tail_live = 0 for the other kernels)
             const unsigned fm = __ballot_sync(kFull, fin);
             if (fm && lane == __ffs(fm) - 1) atomicAdd(P.done, (unsigned long long)__popc(fm));
             fin = false;

@@ -48,7 +48,14 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum",
         "smsp__inst_executed_op_global_red.sum",
         "lts__t_requests_srcunit_tex_op_red.sum",
-        "smsp__average_warp_latency_per_inst_issued.ratio"]
+        "smsp__average_warp_latency_per_inst_issued.ratio",
+        # pipes (round 2: with the 64-byte nodes the ALU pipe, not L1, is the busiest unit)
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "smsp__inst_executed_op_local_ld.sum", "smsp__inst_executed_op_local_st.sum"]
 
 
 def launches(path):
@@ -99,7 +106,21 @@ def main():
     wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
     outdir = os.environ.get("EF_TRAFFIC_DIR", "profiles")   # on the GPU box: a gpurun_out/ subdir
     os.makedirs(outdir, exist_ok=True)
+    def pct(k):
+        try:
+            return float(m[k][0].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+    util = {"issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "l1tex_pct": pct("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l2_pct": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "fp64_pipe_pct": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+            "lanes_per_instruction": pct("smsp__thread_inst_executed_per_inst_executed.ratio"),
+            "warp_instructions": pct("smsp__inst_executed.sum"),
+            "kernel_ms": pct("gpu__time_duration.sum")}
     json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": os.path.basename(rep),
+               "utilisation": util,
                "note": f"one ncu --set full capture of {name.split('(')[0]}"},
               open(os.path.join(outdir, f"traffic_{config}.json"), "w"), indent=1)
     print("\n".join(lines))
