@@ -10,17 +10,9 @@
 
 namespace ef {
 
-// A/B build knobs (tools/build_variant.py): nested push branches (default on),
-// early issue of the next node's loads and extra probe loads (experiments,
-// default off)
+// A/B build knob (tools/build_variant.py): nested push branches (default on)
 #ifndef EF_NESTED_PUSH
 #define EF_NESTED_PUSH 1
-#endif
-#ifndef EF_EARLY_LOAD
-#define EF_EARLY_LOAD 0
-#endif
-#ifndef EF_EXTRA_LOAD
-#define EF_EXTRA_LOAD 0
 #endif
 
 #ifdef EF_PROFILE_PHASES
@@ -645,43 +637,23 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
     int32_t node = 0;
     bool done = false;
     EF_STK_DECL;
-#if EF_EARLY_LOAD
-    F8 X = ldg_f8(nodes->cx), Y = ldg_f8(nodes->cy), Z = ldg_f8(nodes->cz);
-    int4 chn = __ldg(reinterpret_cast<const int4*>(nodes->child));
-#endif
     for (;;) {
         while (node >= 0) {
             EF_PHASE_T0(tv);
 #ifndef EF_NO_WORK_COUNTERS
             ++n_nodes;
 #endif
-            // three 256-bit loads (lo/hi planes of x, y, z), one 128-bit (children)
 #if EF_QNODE
             // two 256-bit loads: x and y plane words, z plane words + children
             const TravNode* q = nodes + node;
             const F8 X = ldg_f8(q->px), Z = ldg_f8(q->pz);
             const int4 ch = make_int4(__float_as_int(Z.e), __float_as_int(Z.f), __float_as_int(Z.g),
                                       __float_as_int(Z.h));
-#elif EF_EARLY_LOAD
-            const int4 ch = chn;
 #else
+            // three 256-bit loads (centres / half extents of x, y, z), one 128-bit (children)
             const TravNode* q = nodes + node;
             const F8 X = ldg_f8(q->cx), Y = ldg_f8(q->cy), Z = ldg_f8(q->cz);
             const int4 ch = __ldg(reinterpret_cast<const int4*>(q->child));
-#if EF_EXTRA_LOAD   // sensitivity probe: one more 16-byte load per node visit (same sector as the children)
-            {
-                int4 junk;
-                asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(junk.x), "=r"(junk.y), "=r"(junk.z), "=r"(junk.w) : "l"(q->pad));
-#if EF_EXTRA_LOAD > 1   // ... and a 32-byte load of another line (the next node's first sector)
-                F8 j2;
-                asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                    : "=f"(j2.a), "=f"(j2.b), "=f"(j2.c), "=f"(j2.d), "=f"(j2.e), "=f"(j2.f), "=f"(j2.g), "=f"(j2.h)
-                    : "l"((q + 1)->cx));
-                n_nodes += (j2.a == 1.2345e-30f) + (j2.h == 1.2345e-30f);
-#endif
-                n_nodes += (junk.x == 0x12345678) + (junk.w == 0x12345678);   // never true: keeps the loads
-            }
-#endif
 #endif
             uint32_t k0, k1, k2, k3;
 #if EF_QNODE
@@ -694,19 +666,6 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             kswap(k0, k2);
             kswap(k1, k3);
             kswap(k1, k2);
-#if EF_EARLY_LOAD
-            // the nearest child's node is fetched before the farther hits are
-            // pushed: the push code runs under the loads' latency (a leaf or
-            // a miss fetches the root: harmless, no branch)
-            const int32_t next = k0 != 0xffffffffu ? pick(ch, k0 & 3u) : -1;
-            {
-                const TravNode* q = nodes + max(next, 0);
-                X = ldg_f8(q->cx);
-                Y = ldg_f8(q->cy);
-                Z = ldg_f8(q->cz);
-                chn = __ldg(reinterpret_cast<const int4*>(q->child));
-            }
-#endif
 #ifdef EF_PROFILE_PHASES
             {
                 const int nh = (k0 != 0xffffffffu) + (k1 != 0xffffffffu) + (k2 != 0xffffffffu) + (k3 != 0xffffffffu);
@@ -741,11 +700,7 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
 #endif
             }
             if (k0 != 0xffffffffu) {
-#if EF_EARLY_LOAD
-                node = next;
-#else
                 node = pick(ch, k0 & 3u);
-#endif
                 EF_PHASE_ADD(0, tv);
                 continue;
             }
@@ -767,15 +722,6 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             }
             EF_PHASE_ADD(0, tv);
             if (done) break;
-#if EF_EARLY_LOAD
-            if (node >= 0) {
-                const TravNode* q = nodes + node;
-                X = ldg_f8(q->cx);
-                Y = ldg_f8(q->cy);
-                Z = ldg_f8(q->cz);
-                chn = __ldg(reinterpret_cast<const int4*>(q->child));
-            }
-#endif
         }
         if (done) {
             EF_STK_FLUSH;
@@ -805,15 +751,6 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             EF_STK(3);
         }
         EF_PHASE_ADD(2, tp);
-#if EF_EARLY_LOAD
-        if (node >= 0) {
-            const TravNode* q = nodes + node;
-            X = ldg_f8(q->cx);
-            Y = ldg_f8(q->cy);
-            Z = ldg_f8(q->cz);
-            chn = __ldg(reinterpret_cast<const int4*>(q->child));
-        }
-#endif
     }
 }
 

@@ -598,8 +598,16 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
 // the shared loop -- and was removed.)
 // SSTACK: the whole traversal stack in shared memory (P.smem_stack >= the
 // tree's max_stack), predicated pushes.
+// CTAs per SM of the split-stack kernel (tuning builds: EF_BIG_CTAS with
+// EF_BIG_THREADS = 1024 / EF_BIG_CTAS)
+#ifndef EF_BIG_CTAS
+#define EF_BIG_CTAS 1
+#endif
+template <bool BRUTE, bool SSTACK>
+constexpr int kCtasPerSm = (!BRUTE && !SSTACK) ? EF_BIG_CTAS : 1;
+
 template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
-__global__ void __launch_bounds__(THREADS, 1) trace_kernel(const TraceParams P) {
+__global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_kernel(const TraceParams P) {
     static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
     static_assert(G == 1 || BRUTE, "lane groups are for the all-pairs path");
     pdl_trigger();   // the tail / analysis kernel may be scheduled onto SMs this grid frees
@@ -942,7 +950,7 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     // Too few paths to give every SM a full CTA (C1: 4,096 paths): spread them
     // over all SMs in smaller CTAs (>= one warp), so each path's latency-bound
     // chain shares its SM with as few others as possible.
-    const long long sms = (long long)sm_count();
+    const long long sms = (long long)sm_count() * kCtasPerSm<BRUTE, SSTACK>;
     const long long lanes = (long long)P.total * G;
     static const int block_env = [] {   // tuning only: threads per CTA (<= THREADS)
         const char* e = std::getenv("EF_BLOCK");
