@@ -364,14 +364,14 @@ struct SegPre {
 // SH histogram commit -> reflection.  With G > 1 the
 // group's lanes split the Philox draws (and diffuse-rain shadow rays on the
 // all-pairs path); everything else runs identically on each lane of the group.
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK, bool FEAT = true>
 __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                                const Hit h, const double* s_tri, uint2* s_stack,
                                                const LaneGroup& lg, const SegPre* pre = nullptr);
 
 // One segment of an active path: closest hit, then finish_segment.  With
 // G > 1 the group's lanes split the closest hit's triangle tests.
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK, bool FEAT>
 __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                               const double* s_tri, uint2* s_stack,
                                               const LaneGroup& lg) {
@@ -390,10 +390,10 @@ __device__ __forceinline__ void trace_segment(const TraceParams& P, PathState<NB
             P.nodes, P.tris, S.ox, S.oy, S.oz, S.dx, S.dy, S.dz, kRayEps, INFINITY, ls.c[EF_ST_NODES],
             ls.c[EF_ST_TRIS], s_stack);
     }
-    finish_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, h, s_tri, s_stack, lg);
+    finish_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK, FEAT>(P, S, ls, h, s_tri, s_stack, lg);
 }
 
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G, bool SSTACK, bool FEAT>
 __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<NBMAX>& S, LaneStats& ls,
                                                const Hit h, const double* s_tri, uint2* s_stack,
                                                const LaneGroup& lg, const SegPre* pre) {
@@ -402,12 +402,12 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
     const bool lead = lg.lead;
     const bool hit = h.id != INT32_MAX;
     EF_PHASE_T0(tsh);
-    if (P.path_ids && !P.timing && lead) P.path_ids[S.path * P.max_bounces + S.nseg] = hit ? h.id : -1;
+    if (FEAT && P.path_ids && !P.timing && lead) P.path_ids[S.path * P.max_bounces + S.nseg] = hit ? h.id : -1;
 
     // ---- listener sphere receiver + SH histogram commit (with diffuse
     // rain, segments leaving a diffuse bounce reach the listener only
     // through the next-event connection: SPEC.md:257, no double count)
-    if (!(P.rain && S.last_diffuse)) {
+    if (!(FEAT && P.rain && S.last_diffuse)) {
         const double Lx = P.lx - S.ox, Ly = P.ly - S.oy, Lz = P.lz - S.oz;
         const double tc = pre ? pre->tc : dot3(Lx, Ly, Lz, S.dx, S.dy, S.dz);
         const double tlim = hit ? h.t : INFINITY;
@@ -415,7 +415,7 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
             const double dist2 = pre ? pre->dist2 : dot3(Lx, Ly, Lz, Lx, Ly, Lz);
             const double perp2 = dist2 - tc * tc;
             if (perp2 <= P.r2 && lead)
-                commit_arrival<NBMAX, ORDER>(P, S.src, S.nrefl, S.tri0, S.tri1, S.plen + tc, -S.dx,
+                commit_arrival<NBMAX, ORDER>(P, S.src, S.nrefl, FEAT ? S.tri0 : -1, FEAT ? S.tri1 : -1, S.plen + tc, -S.dx,
                                              -S.dy, -S.dz, S.E, ls);
         }
     }
@@ -437,8 +437,10 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         S.oy = S.oy + t * S.dy;
         S.oz = S.oz + t * S.dz;
         ++S.nrefl;
-        if (S.nrefl == 1) S.tri0 = h.id;
-        if (S.nrefl == 2) S.tri1 = h.id;
+        if (FEAT) {   // (the ER list's first two reflectors)
+            if (S.nrefl == 1) S.tri0 = h.id;
+            if (S.nrefl == 2) S.tri1 = h.id;
+        }
         ls.c[EF_ST_REFLECTIONS]++;
         // one 48-byte shading record, one level of loads: normal, p_m, material
 #if EF_SHADE64
@@ -470,7 +472,7 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
         const long long fb = clock64();   // shading record + draws
         if (G == 32 && lead) atomicAdd(&g_phase[1], (unsigned long long)(fb - fa));
 #endif
-        if (P.rain && diffuse) {
+        if (FEAT && P.rain && diffuse) {
             // ---- diffuse rain: connect this bounce to the listener
             // centre; Lambertian lobe through the receiver cross-section:
             // c_b = E_b (1-a_b) s_b cos(theta) r^2 / d^2
@@ -507,7 +509,7 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
 #pragma unroll
                     for (int b = 0; b < NBMAX; ++b)
                         c[b] = b < nb ? S.E[b] * __ldg(P.fr + m * nb + b) * gf : 0.f;
-                    commit_arrival<NBMAX, ORDER>(P, S.src, S.nrefl, S.tri0, S.tri1, S.plen + dd, -ex,
+                    commit_arrival<NBMAX, ORDER>(P, S.src, S.nrefl, FEAT ? S.tri0 : -1, FEAT ? S.tri1 : -1, S.plen + dd, -ex,
                                                  -ey, -ez, c, ls);
                 }
             }
@@ -570,10 +572,10 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
 #ifdef EF_PROFILE_PHASES
     if (lead) atomicAdd(&g_phase[4], 1ull);
 #endif
-    if (!S.active && P.path_nseg && lead) P.path_nseg[S.path] = S.nseg;
-    if (P.timing && lead && 5 + S.nseg < P.max_bounces)   // debug: ns since path start, per segment
+    if (FEAT && !S.active && P.path_nseg && lead) P.path_nseg[S.path] = S.nseg;
+    if (FEAT && P.timing && lead && 5 + S.nseg < P.max_bounces)   // debug: ns since path start, per segment
         P.path_ids[S.path * P.max_bounces + 5 + S.nseg] = (int32_t)(globaltimer() - S.t_start);
-    if (!S.active && P.timing && lead) {
+    if (FEAT && !S.active && P.timing && lead) {
         const unsigned long long t_end = globaltimer();
         int32_t* row = P.path_ids + S.path * P.max_bounces;
         unsigned smid;
@@ -606,8 +608,9 @@ __device__ __forceinline__ void finish_segment(const TraceParams& P, PathState<N
 template <bool BRUTE, bool SSTACK>
 constexpr int kCtasPerSm = (!BRUTE && !SSTACK) ? EF_BIG_CTAS : 1;
 
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
-__global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_kernel(const TraceParams P) {
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false, bool FEAT = true>
+__global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_kernel(const TraceParams P_in) {
+    const TraceParams& P = P_in;
     static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
     static_assert(G == 1 || BRUTE, "lane groups are for the all-pairs path");
     pdl_trigger();   // the tail / analysis kernel may be scheduled onto SMs this grid frees
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_ke
                         ls.src = S.src;
                     }
                     ls.c[EF_ST_PATHS]++;
-                    if (P.timing) S.t_start = globaltimer();
+                    if (FEAT && P.timing) S.t_start = globaltimer();
                     S.active = true;
                 }
             }
@@ -720,11 +723,11 @@ __global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_ke
         if (!live) break;
 #ifndef EF_PROFILE_PHASES
         if (!S.active) continue;
-        trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, s_tri, s_stack, lg);
+        trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK, FEAT>(P, S, ls, s_tri, s_stack, lg);
 #else
         const uint32_t n0 = ls.c[EF_ST_NODES], t0 = ls.c[EF_ST_TRIS];
         const bool was = S.active;
-        if (S.active) trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>(P, S, ls, s_tri, s_stack, lg);
+        if (S.active) trace_segment<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK, FEAT>(P, S, ls, s_tri, s_stack, lg);
         {   // SIMT cost of per-lane traversal lengths: 5 sum of node visits,
             // 6 sum over warp-segments of max visits x 32, 7 the same for
             // triangle tests (8 their sum), 9 segments (active lanes)
@@ -943,7 +946,7 @@ static int sm_count() {
     return n;
 }
 
-template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
+template <int NBMAX, int ORDER, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false, bool FEAT = true>
 static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     TraceParams P = P0;
     if (!SSTACK) P.smem_stack = kSplitDepth<THREADS>;   // else: the tree's max_stack
@@ -963,7 +966,7 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     }
     size_t smem = (size_t)P.n_src * (EF_ST_COUNT * 4 + 8) + (BRUTE ? (size_t)P.n_tri * 72 : 0) + 32 +
                   (BRUTE ? 0 : (size_t)P.smem_stack * THREADS * sizeof(uint2));   // THREADS columns
-    auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK>;
+    auto kern = trace_kernel<NBMAX, ORDER, BRUTE, THREADS, G, SSTACK, FEAT>;
     static bool attr_done = false;   // once per instantiation: no per-launch host queries
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -981,14 +984,14 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int NBMAX, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false>
+template <int NBMAX, bool BRUTE, int THREADS, int G = 1, bool SSTACK = false, bool FEAT = true>
 static cudaError_t dispatch_order(int order, const TraceParams& P, cudaStream_t st) {
     switch (order) {
-        case 0: return launch_trace<NBMAX, 0, BRUTE, THREADS, G, SSTACK>(P, st);
-        case 1: return launch_trace<NBMAX, 1, BRUTE, THREADS, G, SSTACK>(P, st);
-        case 2: return launch_trace<NBMAX, 2, BRUTE, THREADS, G, SSTACK>(P, st);
-        case 3: return launch_trace<NBMAX, 3, BRUTE, THREADS, G, SSTACK>(P, st);
-        default: return launch_trace<NBMAX, 4, BRUTE, THREADS, G, SSTACK>(P, st);
+        case 0: return launch_trace<NBMAX, 0, BRUTE, THREADS, G, SSTACK, FEAT>(P, st);
+        case 1: return launch_trace<NBMAX, 1, BRUTE, THREADS, G, SSTACK, FEAT>(P, st);
+        case 2: return launch_trace<NBMAX, 2, BRUTE, THREADS, G, SSTACK, FEAT>(P, st);
+        case 3: return launch_trace<NBMAX, 3, BRUTE, THREADS, G, SSTACK, FEAT>(P, st);
+        default: return launch_trace<NBMAX, 4, BRUTE, THREADS, G, SSTACK, FEAT>(P, st);
     }
 }
 
@@ -1060,8 +1063,15 @@ static cudaError_t dispatch_brute(int order, const TraceParams& P, cudaStream_t 
 template <int NBMAX>
 static cudaError_t dispatch_bvh(bool big, int order, const TraceParams& P, cudaStream_t st) {
     (void)big;
-    if (P.smem_stack > 0) return dispatch_order<NBMAX, false, kSmallThreads, 1, true>(order, P, st);
-    return dispatch_order<NBMAX, false, kBigThreads>(order, P, st);
+    // FEAT = false: the production frame -- no per-path records, timing,
+    // diffuse rain or ER list compiled in (their state and checks cost the
+    // 64-register kernel 4.5%: C5 4.29 -> 4.49, C3 3.15 -> 3.29 G seg/s)
+    const bool feat = P.path_ids || P.path_nseg || P.timing || P.rain || P.er_max_order > 0;
+    if (P.smem_stack > 0)
+        return feat ? dispatch_order<NBMAX, false, kSmallThreads, 1, true, true>(order, P, st)
+                    : dispatch_order<NBMAX, false, kSmallThreads, 1, true, false>(order, P, st);
+    return feat ? dispatch_order<NBMAX, false, kBigThreads, 1, false, true>(order, P, st)
+                : dispatch_order<NBMAX, false, kBigThreads, 1, false, false>(order, P, st);
 }
 
 // Defined one per translation unit (ef_trace_{brute,bvh}_nb{4,8}.cu).

@@ -71,11 +71,21 @@ def _arrivals_parity(name, scan, want):
         assert np.array_equal(tr.path_nseg.cpu().numpy()[0], ref.nseg)
         assert np.array_equal(tr.path_ids.cpu().numpy()[0], ref.ids)
         H, D = tr.irs()[0].numpy()
+        # the production instantiation (no per-path records compiled in: the
+        # kernel the bench times) on the same rays: same counters, same IR
+        tp = propagation.FrameTracer(sc, 1, _cfg(w))
+        tp.set_sources(w.sources[[s]], [s])
+        tp.trace(w.listener, ray_ids=rays)
+        torch.cuda.synchronize()
+        assert torch.equal(tp.stats.cpu(), tr.stats.cpu())
+        Hp, Dp = tp.irs()[0].numpy()
         if np.abs(ref.H).sum() > 0:
             hist_close(H, ref.H)
+            hist_close(Hp, ref.H)
             checked += 1
         if np.abs(ref.Dir).sum() > 0:
             np.testing.assert_allclose(D, ref.Dir, rtol=1e-5, atol=1e-6 * np.abs(ref.Dir).max())
+            np.testing.assert_allclose(Dp, ref.Dir, rtol=1e-5, atol=1e-6 * np.abs(ref.Dir).max())
             checked += 1
     assert checked > 0, "no arriving ray found"
 
