@@ -207,17 +207,20 @@ struct __align__(32) F8 {
 struct __align__(32) D4 {
     double x, y, z, w;
 };
-// L1 policy hints of the node / triangle loads: the triangle records
-// (tested ~3 per segment, rarely reused from L1) skip L1 allocation so the
-// node working set stays (C5 3.92 vs 3.88, C3 2.42 vs 2.40 G seg/s, r02t;
-// evict_first 3.87, evict_last on the nodes 3.88).  Tuning builds:
+// L1 policy hints of the node / triangle loads.  With the 128-byte f32
+// nodes at 512 threads the triangle records (tested ~3 per segment) did
+// best skipping L1 allocation (C5 3.92 vs 3.88, r02t); with the 64-byte
+// nodes at 1024 threads L1 has room for them and the streets' facades are
+// hit again and again: L1::evict_first 4.76, plain 4.75, no_allocate 4.51
+// G seg/s on C5 (C3 3.29 / 3.29 / 3.30, C2 1.74 / 1.75 / 1.72; A/B abI);
+// evict_last on the nodes changes nothing.  Tuning builds:
 // EF_NODE_HINT 1 = L1::evict_last; EF_TRI_HINT 0 = none, 1 = L1::no_allocate,
 // 2 = L1::evict_first
 #ifndef EF_NODE_HINT
 #define EF_NODE_HINT 0
 #endif
 #ifndef EF_TRI_HINT
-#define EF_TRI_HINT 1
+#define EF_TRI_HINT 2
 #endif
 #if EF_NODE_HINT == 1
 #define EF_NODE_Q ".L1::evict_last"
