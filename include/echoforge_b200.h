@@ -96,8 +96,10 @@ uint64_t ef_launch_count(void);
  * (n_tri,3) f64 exactly as the reference stores them (scene.py:152-166),
  * material_index (n_tri,) i64, absorption/scattering (n_materials, n_bands)
  * f64 in [0,1] (scene.py:167-170; n_bands generalised from 4 to 1..8).
- * Builds the device BVH (binned SAH, 128-byte four-child nodes, conservative
- * f32 boxes) and uploads the f64 triangle payload in leaf order. */
+ * Builds the device BVH (binned SAH, four-child nodes with conservative f32
+ * boxes, re-encoded for traversal as 64-byte nodes of 16-bit planes on a
+ * grid over the scene bounds) and uploads the f64 triangle payload in leaf
+ * order. */
 int ef_scene_create(const double* v0, const double* e1, const double* e2,
                     const double* normals, const int64_t* material_index, int64_t n_tri,
                     const double* absorption, const double* scattering,

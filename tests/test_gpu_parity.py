@@ -98,6 +98,46 @@ def test_soup_bvh_vs_reference(golden):
                                       g["v0"], g["e1"], g["e2"]), i
 
 
+def test_quantized_nodes_far_and_axis_parallel_rays(golden):
+    """The 64-byte traversal nodes (16-bit planes on a grid over the scene
+    bounds) stay conservative away from the comfortable case:
+    origins up to 100 scene extents outside the grid, axis-parallel
+    directions (1/d clamped at 1e20), rays grazing the bounds.  Closest hits
+    through the BVH must equal the exact all-pairs answer of the same device
+    test (mode 1), id and t bit for bit."""
+    g = golden("soup700")
+    s = _scene_from_golden(g)
+    rng = np.random.default_rng(11)
+    lo = np.minimum(g["v0"], np.minimum(g["v0"] + g["e1"], g["v0"] + g["e2"])).min(0)
+    hi = np.maximum(g["v0"], np.maximum(g["v0"] + g["e1"], g["v0"] + g["e2"])).max(0)
+    ext = float((hi - lo).max())
+    n = 6000
+    target = rng.uniform(lo, hi, size=(n, 3))
+    dirs = rng.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1)[:, None]
+    dist = ext * 10.0 ** rng.uniform(-1, np.log10(100.0), size=n)   # 0.1 .. 100 extents away
+    o_far = target - dirs * dist[:, None]
+    # axis-parallel rays through the scene, from outside and from inside
+    ax = np.zeros((n, 3))
+    k = rng.integers(0, 3, size=n)
+    ax[np.arange(n), k] = rng.choice([-1.0, 1.0], size=n)
+    o_ax = rng.uniform(lo, hi, size=(n, 3)) - ax * ext * rng.choice([0.0, 1.5, 50.0], size=n)[:, None]
+    # rays along the faces of the bounding box
+    o_gr = rng.uniform(lo, hi, size=(n, 3))
+    o_gr[np.arange(n), k] = np.where(rng.random(n) < 0.5, lo[k], hi[k])
+    d_gr = rng.normal(size=(n, 3))
+    d_gr[np.arange(n), k] = 0.0
+    d_gr /= np.linalg.norm(d_gr, axis=1)[:, None]
+    hits = 0
+    for o, d in ((o_far, dirs), (o_ax, ax), (o_gr, d_gr)):
+        t, tri, hit = s.bvh.intersect_batch(o, d, 1e-4)
+        tb, trib, hitb = s._query(o, d, 1e-4, None, 1)
+        assert np.array_equal(tri, trib)
+        assert np.array_equal(t[hit], tb[hitb])
+        hits += int(hit.sum())
+    assert hits > 3000
+
+
 def test_city_bvh_queries(golden):
     g = golden("c2_city")
     s = _scene_from_golden(g)
