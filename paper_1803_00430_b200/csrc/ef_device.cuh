@@ -14,6 +14,9 @@ namespace ef {
 #ifndef EF_NESTED_PUSH
 #define EF_NESTED_PUSH 1
 #endif
+#ifndef EF_KEY_LOP3
+#define EF_KEY_LOP3 1
+#endif
 
 #ifdef EF_PROFILE_PHASES
 // debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
@@ -415,6 +418,21 @@ __device__ __forceinline__ uint32_t slab_key_ce(float nx, float fx, float ny, fl
     return tn <= tf ? ((__float_as_uint(tn) & ~3u) | slot) : 0xffffffffu;
 }
 
+#if EF_KEY_LOP3
+// The same key with (bits & ~3) | slot as ONE three-input LOP3: the mask
+// comes in a register the compiler cannot fold (an immediate mask plus an
+// immediate slot would need two instructions).
+template <uint32_t SLOT>
+__device__ __forceinline__ uint32_t slab_key_m(float nx, float fx, float ny, float fy, float nz, float fz,
+                                               float tmin, float tmax, uint32_t mask) {
+    const float tn = fmax3f(nx, ny, fmaxf(nz, tmin));
+    const float tf = fmin3f(fx, fy, fminf(fz, tmax));
+    uint32_t k;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(k) : "r"(__float_as_uint(tn)), "r"(mask), "n"(SLOT));
+    return tn <= tf ? k : 0xffffffffu;
+}
+#endif
+
 // The four children's sortable keys of one node visit (X, Y, Z: the node's
 // three 32-byte plane groups).
 __device__ __forceinline__ void node_keys(const RayF& r, const F8& X, const F8& Y, const F8& Z, float tmin,
@@ -452,6 +470,9 @@ struct RayQ {
     float sx, sy, sz;
     float Bx, By, Bz;
     uint32_t selx, sely, selz;
+#if EF_KEY_LOP3
+    uint32_t mask;
+#endif
 };
 
 __device__ __forceinline__ RayQ make_rayq(const RayF& r, const F8& G) {
@@ -465,6 +486,9 @@ __device__ __forceinline__ RayQ make_rayq(const RayF& r, const F8& G) {
     q.selx = r.ix >= 0.0f ? 0x7410u : 0x7432u;
     q.sely = r.iy >= 0.0f ? 0x7410u : 0x7432u;
     q.selz = r.iz >= 0.0f ? 0x7410u : 0x7432u;
+#if EF_KEY_LOP3
+    asm volatile("mov.u32 %0, 0xfffffffc;" : "=r"(q.mask));
+#endif
     return q;
 }
 
@@ -492,10 +516,17 @@ __device__ __forceinline__ void node_keys_q(const RayQ& r, const F8& A, const F8
     slab_q4(A.a, A.b, A.c, A.d, r.selx, r.sx, r.Bx, nx, fx);
     slab_q4(A.e, A.f, A.g, A.h, r.sely, r.sy, r.By, ny, fy);
     slab_q4(Bz.a, Bz.b, Bz.c, Bz.d, r.selz, r.sz, r.Bz, nz, fz);
+#if EF_KEY_LOP3
+    k0 = slab_key_m<0u>(nx[0], fx[0], ny[0], fy[0], nz[0], fz[0], tmin, tmax, r.mask);
+    k1 = slab_key_m<1u>(nx[1], fx[1], ny[1], fy[1], nz[1], fz[1], tmin, tmax, r.mask);
+    k2 = slab_key_m<2u>(nx[2], fx[2], ny[2], fy[2], nz[2], fz[2], tmin, tmax, r.mask);
+    k3 = slab_key_m<3u>(nx[3], fx[3], ny[3], fy[3], nz[3], fz[3], tmin, tmax, r.mask);
+#else
     k0 = slab_key_ce(nx[0], fx[0], ny[0], fy[0], nz[0], fz[0], tmin, tmax, 0u);
     k1 = slab_key_ce(nx[1], fx[1], ny[1], fy[1], nz[1], fz[1], tmin, tmax, 1u);
     k2 = slab_key_ce(nx[2], fx[2], ny[2], fy[2], nz[2], fz[2], tmin, tmax, 2u);
     k3 = slab_key_ce(nx[3], fx[3], ny[3], fy[3], nz[3], fz[3], tmin, tmax, 3u);
+#endif
 }
 #endif
 

@@ -972,6 +972,8 @@ static cudaError_t launch_trace(const TraceParams& P0, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kMaxTraceSmem);
         if (e != cudaSuccess) return e;
+        if (const char* c = std::getenv("EF_CARVEOUT"))   // tuning: shared-memory carve-out (percent of the SM's 228 KB)
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
         attr_done = true;
     }
     if (smem > kMaxTraceSmem) return cudaErrorInvalidValue;
