@@ -577,34 +577,49 @@ __device__ __forceinline__ void leaf_test(const GpuTri* __restrict__ tris, int32
 // on every push and pop: ~13% of the C5 kernel's instructions, r02c.)
 constexpr int kSmemStack = 16;   // max shared entries per thread
 
-// Shared top (DEPTH entries) + local-memory overflow (rarely touched).
+// Shared-window address of the dynamic shared memory of a kernel without
+// static shared memory (sm_100a reserves the first 1 KB of the window).  The
+// split-stack trace kernel checks it once at its start and traps otherwise.
+constexpr uint32_t kDynSmemBase = 0x400u;
+
+// Shared top (DEPTH entries) + local-memory overflow (rarely touched).  The
+// whole stack pointer is ONE register: sa = kDynSmemBase + 8 t + sp * STEP,
+// the shared address of entry sp of thread t (the stack area opens the
+// kernel's dynamic shared memory, 8 t < STEP).  Emptiness, the shared /
+// local split and the entry index are all compares of sa with immediates.
+// (With a (column base, sp) pair the compiler, at 64 registers, rebuilt the
+// column base on every push and pop -- S2R tid, S2UR cta id, UMOV, ULEA, LEA,
+// IMAD: 3.7% of the C5 kernel's instructions at 4 active lanes, r02 source
+// view.)
 template <int DEPTH, uint32_t STEP>
 struct StackSplit {
     static constexpr bool kPredicated = false;
-    uint32_t sbase;  // shared address of this thread's column
-    int sp;
+    static constexpr uint32_t kLo = kDynSmemBase + STEP;           // sa < kLo: empty
+    static constexpr uint32_t kHi = kDynSmemBase + DEPTH * STEP;   // sa < kHi: entry in shared memory
+    uint32_t sa;
     uint2* l;        // local-memory overflow array (outside the struct, so the
-                     // scalars can live in registers)
+                     // scalar can live in a register)
 
+    __device__ __forceinline__ bool empty() const { return sa < kLo; }
+    __device__ __forceinline__ int depth() const { return (int)((sa - kDynSmemBase) / STEP); }
+    __device__ __forceinline__ void pop() { sa -= STEP; }
     __device__ __forceinline__ void push(int32_t node, uint32_t key) {
-        if (sp < DEPTH) {
+        if (sa < kHi) {
             // volatile asm keeps push/pop order; no memory clobber, so global
             // loads (nodes, triangles) still schedule freely around it
-            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sbase + (uint32_t)sp * STEP),
-                         "r"((uint32_t)node), "r"(key));
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sa), "r"((uint32_t)node), "r"(key));
         } else {
-            l[sp] = make_uint2((uint32_t)node, key);
+            l[depth()] = make_uint2((uint32_t)node, key);
         }
-        ++sp;
+        sa += STEP;
     }
     __device__ __forceinline__ uint2 top() const {
-        if (sp < DEPTH) {
+        if (sa < kHi) {
             uint2 e;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
-                         : "r"(sbase + (uint32_t)sp * STEP));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(sa));
             return e;
         }
-        return l[sp];
+        return l[depth()];
     }
 };
 
@@ -616,6 +631,9 @@ struct StackShared {
     uint32_t sbase;
     int sp;
 
+    __device__ __forceinline__ bool empty() const { return sp == 0; }
+    __device__ __forceinline__ int depth() const { return sp; }
+    __device__ __forceinline__ void pop() { --sp; }
     // push `node, key` if `valid` (no branch: predicated st.shared)
     __device__ __forceinline__ void push_if(int32_t node, uint32_t key, bool valid) {
         asm volatile(
@@ -637,6 +655,9 @@ struct StackLocal {
     static constexpr bool kPredicated = false;
     uint2 l[kStackSize];
     int sp;
+    __device__ __forceinline__ bool empty() const { return sp == 0; }
+    __device__ __forceinline__ int depth() const { return sp; }
+    __device__ __forceinline__ void pop() { --sp; }
     __device__ __forceinline__ void push(int32_t node, uint32_t key) {
         l[sp++] = make_uint2((uint32_t)node, key);
     }
@@ -707,7 +728,7 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
                 if (nh > 1) {
                     stk[0] += nh - 1;
                     for (int i_ = 0; i_ < nh - 1; ++i_)
-                        if (st.sp + i_ >= EF_SPLIT_DEPTH_PROBE) EF_STK(1);
+                        if (st.depth() + i_ >= EF_SPLIT_DEPTH_PROBE) EF_STK(1);
                 }
             }
 #endif
@@ -741,11 +762,11 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
             // no child hit: pop the next node still in front of the closest
             // hit (the key's t is rounded down, so the cull is conservative)
             for (;;) {
-                if (st.sp == 0) {
+                if (st.empty()) {
                     done = true;
                     break;
                 }
-                --st.sp;
+                st.pop();
                 const uint2 e = st.top();
                 if (__uint_as_float(e.y & ~3u) <= tb) {
                     node = (int32_t)e.x;
@@ -771,11 +792,11 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
         }
         EF_PHASE_T0(tp);
         for (;;) {
-            if (st.sp == 0) {
+            if (st.empty()) {
                 EF_STK_FLUSH;
                 return h;
             }
-            --st.sp;
+            st.pop();
             const uint2 e = st.top();
             if (__uint_as_float(e.y & ~3u) <= tb) {
                 node = (int32_t)e.x;
@@ -802,7 +823,8 @@ __device__ __forceinline__ Hit closest_bvh_column(const TravNode* __restrict__ n
         return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
     } else {
         uint2 overflow[kStackSize];
-        StackSplit<DEPTH, 8u * THREADS> st{stack_column(s_stack), 0, overflow};
+        (void)s_stack;   // the stack area opens the dynamic shared memory (checked by the kernel)
+        StackSplit<DEPTH, 8u * THREADS> st{kDynSmemBase + 8u * threadIdx.x, overflow};
         return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
     }
 }
