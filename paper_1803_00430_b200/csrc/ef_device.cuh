@@ -536,10 +536,29 @@ __device__ __forceinline__ void kswap(uint32_t& a, uint32_t& b) {
     b = hi;
 }
 
+// Child `slot` (the low two bits of a sort key) of a node: a two-level
+// select, no branches.  In PTX so that each bit test is an and + setp.ne 0
+// (one LOP3 with a predicate result each); the C++ form's i1 truncation of
+// bit 0 became and + setp.eq 1, two instructions.
+#ifndef EF_PICK_PTX
+#define EF_PICK_PTX 1
+#endif
 __device__ __forceinline__ int32_t pick(const int4& c, uint32_t slot) {
-    const int32_t a = (slot & 1u) ? c.y : c.x;   // two-level select, no branches
+#if EF_PICK_PTX
+    int32_t r;
+    asm("{\n\t.reg .pred p0, p1;\n\t.reg .b32 t0, t1, a, b;\n\t"
+        "and.b32 t0, %5, 1;\n\tsetp.ne.u32 p0, t0, 0;\n\t"
+        "and.b32 t1, %5, 2;\n\tsetp.ne.u32 p1, t1, 0;\n\t"
+        "selp.b32 a, %2, %1, p0;\n\tselp.b32 b, %4, %3, p0;\n\t"
+        "selp.b32 %0, b, a, p1;\n\t}"
+        : "=r"(r)
+        : "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w), "r"(slot));
+    return r;
+#else
+    const int32_t a = (slot & 1u) ? c.y : c.x;
     const int32_t b = (slot & 1u) ? c.w : c.z;
     return (slot & 2u) ? b : a;
+#endif
 }
 
 // Leaf: exact tests of up to 8 consecutive triangles of the leaf-ordered
@@ -794,7 +813,7 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
         for (;;) {
             if (st.empty()) {
                 EF_STK_FLUSH;
-                return h;
+                    return h;
             }
             st.pop();
             const uint2 e = st.top();
