@@ -643,28 +643,29 @@ struct StackSplit {
 };
 
 // The whole stack in shared memory (the host guarantees the column holds the
-// tree's max_stack): pushes are predicated stores, no overflow branch.
+// tree's max_stack): pushes are predicated stores, no overflow branch.  Like
+// StackSplit the pointer is one register, the shared address of the next
+// entry (8 t < STEP).
 template <uint32_t STEP>
 struct StackShared {
     static constexpr bool kPredicated = true;
-    uint32_t sbase;
-    int sp;
+    static constexpr uint32_t kLo = kDynSmemBase + STEP;   // sa < kLo: empty
+    uint32_t sa;
 
-    __device__ __forceinline__ bool empty() const { return sp == 0; }
-    __device__ __forceinline__ int depth() const { return sp; }
-    __device__ __forceinline__ void pop() { --sp; }
+    __device__ __forceinline__ bool empty() const { return sa < kLo; }
+    __device__ __forceinline__ int depth() const { return (int)((sa - kDynSmemBase) / STEP); }
+    __device__ __forceinline__ void pop() { sa -= STEP; }
     // push `node, key` if `valid` (no branch: predicated st.shared)
     __device__ __forceinline__ void push_if(int32_t node, uint32_t key, bool valid) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-            "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(sbase + (uint32_t)sp * STEP),
+            "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(sa),
             "r"((uint32_t)node), "r"(key), "r"((uint32_t)valid));
-        sp += valid ? 1 : 0;
+        sa += valid ? STEP : 0u;
     }
     __device__ __forceinline__ uint2 top() const {
         uint2 e;
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
-                     : "r"(sbase + (uint32_t)sp * STEP));
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(sa));
         return e;
     }
 };
@@ -682,11 +683,6 @@ struct StackLocal {
     }
     __device__ __forceinline__ uint2 top() const { return l[sp]; }
 };
-
-// shared-window address of this thread's column of the stack area s_stack
-__device__ __forceinline__ uint32_t stack_column(const uint2* s_stack) {
-    return (uint32_t)__cvta_generic_to_shared(s_stack) + 8u * threadIdx.x;
-}
 
 // Closest hit over the 4-wide device BVH.  Accepts t in (t_min, t_max];
 // equal t resolves to the lowest triangle id, so the answer is independent of
@@ -838,7 +834,8 @@ __device__ __forceinline__ Hit closest_bvh_column(const TravNode* __restrict__ n
                                                   uint32_t& n_nodes, uint32_t& n_tris,
                                                   const uint2* s_stack, bool any_hit = false) {
     if constexpr (SSTACK) {
-        StackShared<8u * THREADS> st{stack_column(s_stack), 0};
+        (void)s_stack;
+        StackShared<8u * THREADS> st{kDynSmemBase + 8u * threadIdx.x};
         return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
     } else {
         uint2 overflow[kStackSize];

@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(THREADS, (kCtasPerSm<BRUTE, SSTACK>)) trace_ke
     // counters (f64 path-length sums, u32 counters: a block's per-source
     // counts stay far below 2^32) and the all-pairs triangles
     uint2* s_stack = reinterpret_cast<uint2*>(smem);
-    if constexpr (!BRUTE && !SSTACK) {   // StackSplit addresses its columns from this constant
+    if constexpr (!BRUTE) {   // the stacks address their columns from this constant
         if ((uint32_t)__cvta_generic_to_shared(smem) != kDynSmemBase) __trap();
     }
     const uint32_t stack_bytes = BRUTE ? 0u : (uint32_t)P.smem_stack * THREADS * 8u;
