@@ -196,6 +196,37 @@ extern "C" int ef_eval_sh_batch(const double* dirs, int64_t n, int32_t order, do
 
 namespace {
 
+// The BVH trace kernels address their shared-memory stack columns from the
+// constant kDynSmemBase (ef_device.cuh) and trap if their dynamic shared
+// memory starts elsewhere.  A one-time probe (a kernel without static shared
+// memory, like them) turns that into an error message before the first BVH
+// trace of the process; it is not counted as a launch of the path.
+__global__ void smem_base_probe(uint32_t* out) {
+    extern __shared__ unsigned char probe_smem[];
+    *out = (uint32_t)__cvta_generic_to_shared(probe_smem);
+}
+
+int check_smem_base() {
+    static bool probed = false;
+    static uint32_t base = 0;
+    if (!probed) {
+        uint32_t* d = nullptr;
+        cudaError_t e = cudaMalloc(&d, sizeof(uint32_t));
+        if (e == cudaSuccess) {
+            smem_base_probe<<<1, 1, 16>>>(d);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaMemcpy(&base, d, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+            cudaFree(d);
+        }
+        if (e != cudaSuccess) return check_cuda(e, "smem_base_probe");   // probed again by the next call
+        probed = true;
+    }
+    if (base == kDynSmemBase) return EF_OK;
+    return set_error(EF_EUNSUPPORTED, "ef_trace: dynamic shared memory starts at window address " +
+                                          std::to_string(base) + ", the kernels were built for " +
+                                          std::to_string(kDynSmemBase) + " (kDynSmemBase, ef_device.cuh)");
+}
+
 // ef_trace and ef_trace_fused: either local H/Dir, or the ranks' blocks
 // Hp/Dp (host arrays of n_ranks device pointers) with `spr` sources per rank
 // (H = Dir = null).
@@ -223,6 +254,10 @@ int trace_impl(const ef_scene* s, const ef_trace_config* cfg, const double* src_
     if (s->n_tri == 0) return set_error(EF_EUNSUPPORTED, "ef_trace: empty scene is handled by the host");
     const bool brute = cfg->mode == 1 || (cfg->mode == 0 && s->n_tri <= kBruteMaxTris);
     if (brute && s->n_tri > 2048) return set_error(EF_EINVAL, "ef_trace: all-pairs mode supports <= 2048 triangles");
+    if (!brute) {
+        const int rc = check_smem_base();
+        if (rc != EF_OK) return rc;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const int nk = (cfg->order + 1) * (cfg->order + 1);
     cudaError_t e = cudaSuccess;
