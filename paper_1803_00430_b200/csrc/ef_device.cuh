@@ -22,7 +22,9 @@ namespace ef {
 // debug builds only: clock64 cycles per phase (0 inner visits, 1 leaves,
 // 2 pops after leaves, 3 shading, 4 segments)
 constexpr int kPhaseSlots = 24;
-#define EF_SPLIT_DEPTH_PROBE 12
+#ifndef EF_SPLIT_DEPTH_PROBE
+#define EF_SPLIT_DEPTH_PROBE 12   // stack depth whose crossing the probe counts ("past the shared top")
+#endif
 static __device__ unsigned long long g_phase[kPhaseSlots];   // per translation unit
 #define EF_PHASE_T0(v) const long long v = clock64()
 #define EF_PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(clock64() - (v)))

@@ -460,6 +460,38 @@ def test_mean_free_path_shoebox():
     assert abs(st.mean_free_path - 4 * 1000 / 600) / (4 * 1000 / 600) < 0.03
 
 
+def test_soup_through_split_stack_kernel():
+    """50k overlapping random triangles: a scene beyond kBigSceneBytes, so the
+    1024-thread split-stack kernel traces it, and a ray crosses many
+    overlapping boxes, so its traversal stack overflows the shared top into
+    local memory.  Ids and bounce counts exact outside documented near-ties."""
+    from paper_1803_00430_b200.workloads import Workload
+    rng = np.random.default_rng(77)
+    T = 50_000
+    c = rng.uniform(0.0, 10.0, size=(T, 1, 3))
+    tris = c + rng.normal(scale=0.5, size=(T, 3, 3))
+    w = Workload("soup50k", tris, rng.integers(0, 2, T).astype(np.int64),
+                 np.array([[0.1, 0.2, 0.3, 0.4], [0.3, 0.2, 0.1, 0.05]]),
+                 np.array([[0.5] * 4, [0.2, 0.4, 0.6, 0.8]]),
+                 sources=np.array([[5.0, 5.0, 5.0], [1.0, 2.0, 8.0]]), listener=np.array([6.0, 4.0, 5.0]),
+                 radius=0.5, n_rays=4096, max_bounces=24, order=2, seed=5)
+    n = 768
+    _, _, tr = _run_gpu(w, n_rays=n)
+    os_ = _oracle_for(w)
+    nseg = tr.path_nseg.cpu().numpy()
+    ids = tr.path_ids.cpu().numpy()
+    excl = 0
+    segs = 0
+    for j in range(2):
+        ref = _oracle_trace(os_, w, j, np.arange(n, dtype=np.uint32))
+        bad, e = _compare_paths(nseg[j], ids[j], ref)
+        assert bad == 0, (j, bad)
+        excl += e
+        segs += int(ref.nseg.sum())
+    assert segs > 4 * n          # the paths do bounce through the soup
+    assert excl <= 0.02 * 2 * n
+
+
 @pytest.mark.parametrize("name,n,srcs", [("c3", 256, [0, 5, 17]), ("c5", 512, [0, 100, 255])])
 def test_large_scene_subsample_parity(name, n, srcs):
     """C3 (99k jittered triangles, 8 bands) and C5 (964k triangles): ray
