@@ -600,7 +600,8 @@ constexpr int kSmemStack = 16;   // max shared entries per thread
 
 // Shared-window address of the dynamic shared memory of a kernel without
 // static shared memory (sm_100a reserves the first 1 KB of the window).  The
-// split-stack trace kernel checks it once at its start and traps otherwise.
+// host probes it before the first BVH trace (check_smem_base, ef_trace.cu)
+// and the BVH trace kernels check it at their start and trap otherwise.
 constexpr uint32_t kDynSmemBase = 0x400u;
 
 // Shared top (DEPTH entries) + local-memory overflow (rarely touched).  The
@@ -811,7 +812,7 @@ __device__ __forceinline__ Hit closest_bvh(const TravNode* __restrict__ nodes,
         for (;;) {
             if (st.empty()) {
                 EF_STK_FLUSH;
-                    return h;
+                return h;
             }
             st.pop();
             const uint2 e = st.top();
