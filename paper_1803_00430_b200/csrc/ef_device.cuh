@@ -625,13 +625,18 @@ struct StackSplit {
     __device__ __forceinline__ bool empty() const { return sa < kLo; }
     __device__ __forceinline__ int depth() const { return (int)((sa - kDynSmemBase) / STEP); }
     __device__ __forceinline__ void pop() { sa -= STEP; }
+    // slot of entry sa in the overflow array: sa / STEP is depth() or
+    // depth() + 1 (threads whose 8 t carries into the next STEP), the same
+    // for a thread's push and pop of an entry, so no offset is subtracted;
+    // the array has one spare slot
+    __device__ __forceinline__ uint32_t overflow_slot() const { return sa / STEP; }
     __device__ __forceinline__ void push(int32_t node, uint32_t key) {
         if (sa < kHi) {
             // volatile asm keeps push/pop order; no memory clobber, so global
             // loads (nodes, triangles) still schedule freely around it
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sa), "r"((uint32_t)node), "r"(key));
         } else {
-            l[depth()] = make_uint2((uint32_t)node, key);
+            l[overflow_slot()] = make_uint2((uint32_t)node, key);
         }
         sa += STEP;
     }
@@ -641,7 +646,7 @@ struct StackSplit {
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(sa));
             return e;
         }
-        return l[depth()];
+        return l[overflow_slot()];
     }
 };
 
@@ -841,7 +846,7 @@ __device__ __forceinline__ Hit closest_bvh_column(const TravNode* __restrict__ n
         StackShared<8u * THREADS> st{kDynSmemBase + 8u * threadIdx.x};
         return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
     } else {
-        uint2 overflow[kStackSize];
+        uint2 overflow[kStackSize + 1];
         (void)s_stack;   // the stack area opens the dynamic shared memory (checked by the kernel)
         StackSplit<DEPTH, 8u * THREADS> st{kDynSmemBase + 8u * threadIdx.x, overflow};
         return closest_bvh(nodes, tris, ox, oy, oz, dx, dy, dz, t_min, t_max, n_nodes, n_tris, st, any_hit);
